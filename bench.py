@@ -1,0 +1,442 @@
+#!/usr/bin/env python
+"""rPIE sweep benchmark (BASELINE.json metric: diffraction positions/s per
+rPIE iteration at 256x256x3 modes; % HBM roofline).
+
+Workload (BASELINE.json configs[1]): simulated 20x20 scan
+(400 positions), 256x256 patterns, 3 mixed-state probe modes, rPIE
+(alpha 0.9, beta = gamma = 0.5), far field, shuffled order.  A step is one rPIE
+iteration (one sweep over all 400 positions).  Each GPU runs R independent
+reconstructions of that dataset in exact reference (sequential) order,
+interleaved in one cooperative launch per sweep ("replica mode");
+R = 1 is the single-reconstruction latency figure, also reported.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--replicas R]
+    python bench.py --impl reference ...   # the reference algorithm on host cores
+Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N (one rank per GPU,
+replicas only -- the sequential path does not shard; weak scaling).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+W, M, GRID, STEP_PX, RADIUS = 256, 3, (20, 20), 32.0, 60.0
+POWERS = (0.8, 0.1, 0.1)
+B_POS = W * W * (20 + 16 * M)        # algorithmic bytes per position
+METRIC = "diffraction positions/sec per rPIE iteration at 256x256x3 modes; % HBM roofline"
+WORKLOAD = ("config 2: simulated 20x20 scan (400 positions), 256x256 patterns, 3 mixed-state "
+            "probe modes, rPIE alpha=0.9 beta=gamma=0.5, Fraunhofer, shuffled order")
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def solver_config(precision="fp32"):
+    import paper_2205_04295_b200 as pk
+    return pk.SolverConfig(alpha_obj=0.9, alpha_probe=0.9, beta=0.5, gamma=0.5, mode_count=M,
+                           position_order="shuffled", shuffle_seed=0, precision=precision)
+
+
+def make_dataset(seed=1):
+    import paper_2205_04295_b200 as pk
+    geom = pk.Geometry.create(8.3187e-10, 0.75, 20e-6, W)
+    plan = pk.make_scan(GRID, STEP_PX, 1.0, seed=seed)
+    obj = pk.make_object(pk.canvas_shape_for(plan, W), "spokes", seed=seed)
+    probes = pk.make_probe(pk.ProbeSpec(M, POWERS, "disk", RADIUS), geom)
+    ds = pk.synthesize(obj, probes, plan, geom, noise="none", seed=seed)
+    ds.patterns = ds.patterns.astype(np.float32)          # the container's on-disk precision
+    return ds
+
+
+# ------------------------------------------------------------- clocks ----
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def flush_l2(buf):
+    buf.add_(1)      # 256 MiB read+write > 126 MB L2
+
+
+# ------------------------------------------------------------ GPU arm -----
+def run_states(states, datasets, cfg, kernel_events=None):
+    import paper_2205_04295_b200 as pk
+    pk.sweep_replicas(states, datasets, cfg, kernel_events=kernel_events)
+
+
+def gpu_arm(args, rank, world):
+    import torch
+    import paper_2205_04295_b200 as pk
+    from paper_2205_04295_b200 import _native
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    cfg = solver_config(args.precision)
+    ds = make_dataset(seed=1)
+    n = ds.n_positions
+    R = args.replicas
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def fresh(r):
+        c = pk.SolverConfig(**{**cfg.__dict__, "init_seed": rank * 1000 + r})
+        return pk.initialize(ds, c)
+
+    # ---- value: R replicas resident in HBM, device-timed sweeps
+    states = [fresh(r) for r in range(R)]
+    dsets = [ds] * R
+    for _ in range(args.warmup):
+        run_states(states, dsets, cfg)
+    torch.cuda.synchronize()
+    step_ms, kern_ms = [], []
+    launches0 = _native.launch_count()
+    with ClockSampler(dev.index) as clocks:
+        for _ in range(args.steps):
+            flush_l2(flush)
+            if world > 1:
+                torch.distributed.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            run_states(states, dsets, cfg, kernel_events=(k0, k1))
+            e1.record()
+            torch.cuda.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            kern_ms.append(k0.elapsed_time(k1))
+    launches = _native.launch_count() - launches0
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms, sum(kern_ms)], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms, kern_total = t.tolist()
+    else:
+        kern_total = sum(kern_ms)
+    positions = R * n * args.steps * world
+    value = positions / (total_ms / 1e3)
+    kernel_s = kern_total / 1e3 / args.steps                 # per sweep launch (R*n positions)
+    hbm, peak_kind = peaks()
+    achieved = R * n * B_POS / kernel_s / 1e9
+    traffic = None
+    tp = ROOT / "profiles" / "sweep_traffic.json"
+    if tp.exists():
+        tj = json.loads(tp.read_text())
+        if tj.get("replicas") == R and tj.get("window") == W:
+            traffic = tj.get("dram_bytes_per_launch")
+
+    # ---- single reconstruction (R = 1): the reference's own sequential case
+    single = None
+    if R != 1 and not args.no_single:
+        st1 = [fresh(0)]
+        for _ in range(2):
+            run_states(st1, [ds], cfg)
+        ms1 = []
+        for _ in range(max(3, args.steps // 2)):
+            flush_l2(flush)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            run_states(st1, [ds], cfg)
+            b.record()
+            torch.cuda.synchronize()
+            ms1.append(a.elapsed_time(b))
+        mean1 = statistics.mean(ms1)
+        single = {"positions_per_s": n / (mean1 / 1e3), "iterations_per_s": 1e3 / mean1,
+                  "us_per_visit": mean1 * 1e3 / n, "ms_per_iteration": mean1}
+
+    # ---- e2e: the public API on HOST buffers; H2D of the step's inputs and
+    # D2H of its result inside the timed region, every step
+    e2e = e2e_arm(args, states, ds, cfg, dev, world)
+    return dict(value=value, ms_per_step=total_ms / args.steps, kernel_ms=kern_total / args.steps,
+                achieved=achieved, hbm=hbm, peak_kind=peak_kind, traffic=traffic, clocks=clocks.summary(),
+                launches=launches, single=single, e2e=e2e, n=n)
+
+
+def e2e_arm(args, states, ds, cfg, dev, world):
+    import torch
+    import paper_2205_04295_b200 as pk
+    R = len(states)
+    host_pat = torch.from_numpy(np.ascontiguousarray(ds.patterns, np.float32)).pin_memory()
+    dev_pat = [pk.engine.device_patterns(ds, torch.float32)]
+    # every replica gets its own host copy of the state
+    host_state = []
+    for st in states:
+        host_state.append((st.obj.cpu().pin_memory(), st.probe_stack.cpu().pin_memory(),
+                           st.positions.cpu().pin_memory()))
+    h2d = d2h = 0
+    ms = []
+    for it in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        dev_pat[0].copy_(host_pat, non_blocking=True)
+        bi = host_pat.numel() * 4
+        for st, (ho, hp, hx) in zip(states, host_state):
+            st.obj.copy_(ho, non_blocking=True)
+            st.probe_stack.copy_(hp, non_blocking=True)
+            st.positions.copy_(hx, non_blocking=True)
+            bi += ho.numel() * ho.element_size() + hp.numel() * hp.element_size() + hx.numel() * 8
+        pk.sweep_replicas(states, [ds] * R, cfg)
+        bo = 0
+        for st, (ho, hp, hx) in zip(states, host_state):
+            ho.copy_(st.obj, non_blocking=True)
+            hp.copy_(st.probe_stack, non_blocking=True)
+            hx.copy_(st.positions, non_blocking=True)
+            bo += ho.numel() * ho.element_size() + hp.numel() * hp.element_size() + hx.numel() * 8 + 8
+        b.record()
+        torch.cuda.synchronize()
+        if it >= args.warmup:
+            ms.append(a.elapsed_time(b))
+            h2d, d2h = bi, bo
+    total = sum(ms)
+    if world > 1:
+        t = torch.tensor([total], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total = t.item()
+    value = R * ds.n_positions * args.steps * world / (total / 1e3)
+    return {"value": value, "unit": "positions/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h)}
+
+
+# ------------------------------------------------------- CPU reference ----
+def _cpu_worker(payload):
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    import numpy as _np
+    from oracle import rpie
+    patterns, positions, probes, cfg_kw, sample = payload
+
+    class Cfg:
+        pass
+    cfg = Cfg()
+    for k, v in cfg_kw.items():
+        setattr(cfg, k, v)
+    st = rpie.initialize(patterns, positions, W, cfg)
+    st.probes = [_np.asarray(p, _np.complex128) for p in probes]
+    t0 = time.perf_counter()
+    rpie.sweep(st, patterns, W, cfg, order=_np.arange(sample))
+    return sample, time.perf_counter() - t0
+
+
+def cpu_sample_payload(sample):
+    ds = make_dataset_host(sample)
+    cfg_kw = dict(alpha_obj=0.9, alpha_probe=0.9, beta=0.5, gamma=0.5, mode_count=M,
+                  position_order="fixed", shuffle_seed=0, init_seed=0, epsilon_rel=1e-12,
+                  ortho_interval=0, update_probe_modes=True, posref=None, track_modulus_error=False)
+    return ds, cfg_kw
+
+
+def make_dataset_host(sample):
+    """The first `sample` positions of the config-2 dataset, synthesised on the
+    host with numpy (the reference arm never touches the GPU path)."""
+    import paper_2205_04295_b200.simulate as sim
+    from oracle import rpie
+    import paper_2205_04295_b200 as pk
+    geom = pk.Geometry.create(8.3187e-10, 0.75, 20e-6, W)
+    plan = sim.make_scan(GRID, STEP_PX, 1.0, seed=1)
+    obj = sim.make_object(sim.canvas_shape_for(plan, W), "spokes", seed=1)
+    probes = sim.make_probe(sim.ProbeSpec(M, POWERS, "disk", RADIUS), geom)
+    fy = np.fft.fftfreq(W)[:, None]
+    fx = np.fft.fftfreq(W)[None, :]
+    pats = np.empty((sample, W, W))
+    for j in range(sample):
+        x, y = plan.true_positions[j]
+        ar, ac = int(round(y)), int(round(x))
+        view = obj[ar:ar + W, ac:ac + W]
+        view = np.fft.ifft2(np.fft.fft2(view) * np.exp(-2j * np.pi * (fy * -(y - ar) + fx * -(x - ac))))
+        pats[j] = sum(np.abs(rpie.centered_fft2(p * view)) ** 2 for p in probes)
+    pats = pats.astype(np.float32).astype(np.float64)
+    return pats, np.asarray(plan.nominal[:sample], np.float64)
+
+
+def cpu_reference(workers, sample, repeats):
+    """The reference algorithm (oracle port, numpy float64, one process per core)
+    on `workers` host cores, each sweeping `sample` positions of config 2."""
+    import multiprocessing as mp
+    (pats, pos), cfg_kw = cpu_sample_payload(sample)
+    # initial probes as the reference would build them (mode noise etc.)
+    from oracle import rpie
+
+    class Cfg:
+        pass
+    cfg = Cfg()
+    for k, v in cfg_kw.items():
+        setattr(cfg, k, v)
+    probes = rpie.initialize(pats, pos, W, cfg).probes
+    payload = (pats, pos, probes, cfg_kw, sample)
+    ctx = mp.get_context("spawn")
+    env_threads = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")}
+    for k in env_threads:
+        os.environ[k] = "1"
+    walls = []
+    with ctx.Pool(workers) as pool:
+        pool.map(_cpu_worker, [payload] * workers)               # warm the workers
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            pool.map(_cpu_worker, [payload] * workers)
+            walls.append(time.perf_counter() - t0)
+    for k, v in env_threads.items():
+        if v is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = v
+    return [workers * sample / w for w in walls]
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------ main ----
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--replicas", type=int, default=int(os.environ.get("PTY_BENCH_REPLICAS", 16)))
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--cpu-sample", type=int, default=32)
+    ap.add_argument("--cpu-workers", type=int, default=0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-single", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    cores = host_cores()
+    workers = args.cpu_workers or max(1, min(cores, 64))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        vals = cpu_reference(workers, args.cpu_sample, max(1, args.warmup + args.steps))
+        vals = vals[args.warmup:] or vals
+        v = statistics.mean(vals)
+        line = {"metric": METRIC, "value": v, "unit": "positions/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1e3 * workers * args.cpu_sample / v,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "impl": "reference",
+                "config": {"workload": WORKLOAD, "window": W, "modes": M,
+                           "positions_per_step": workers * args.cpu_sample,
+                           "parallelism": f"{workers} single-thread reference processes"},
+                "cpu_baseline": {"value": v, "unit": "positions/s", "cores": workers, "kind": "port",
+                                 "sample": f"{args.cpu_sample} positions of config 2 per process, "
+                                           f"{workers} processes (oracle/rpie.py numpy float64)"},
+                "e2e": {"value": v, "unit": "positions/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    if world > 1:
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        torch.distributed.init_process_group("nccl")
+    res = gpu_arm(args, rank, world)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        vals = cpu_reference(workers, args.cpu_sample, 1)
+        cpu = {"value": vals[0], "unit": "positions/s", "cores": workers, "kind": "port",
+               "sample": f"{args.cpu_sample} positions of config 2 per process, {workers} "
+                         f"single-thread processes on {cores} host cores (oracle/rpie.py, numpy float64)"}
+    if rank == 0:
+        frac = res["achieved"] / res["hbm"]
+        line = {
+            "metric": METRIC, "value": res["value"], "unit": "positions/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "c64" if args.precision == "fp32" else "c128", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "window": W, "modes": M, "positions": res["n"],
+                       "replicas_per_gpu": args.replicas, "precision": args.precision,
+                       "parallelism": f"replicas x{args.replicas} per GPU x{world} GPUs",
+                       "l2": "256 MiB buffer rewritten between timed steps"},
+            "roofline": {"bound": "hbm", "achieved": res["achieved"], "peak": res["hbm"], "unit": "GB/s",
+                         "frac": frac, "traffic": res["traffic"],
+                         "kernel": "pty::sweep_kernel<float,256> (persistent cooperative sweep)",
+                         "bytes_per_position": B_POS, "peak_kind": res["peak_kind"],
+                         "kernel_ms_per_step": res["kernel_ms"]},
+            "cpu_baseline": cpu,
+            "e2e": res["e2e"],
+            "gpu_launches": res["launches"],
+            "clocks": res["clocks"],
+            "single_reconstruction": res["single"],
+            "iterations_per_s": 1e3 / res["ms_per_step"],
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

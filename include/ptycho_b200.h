@@ -1,0 +1,162 @@
+/*
+ * ptycho_b200.h -- C ABI of the B200 rPIE hot path (libptycho_b200.so).
+ *
+ * Plain pointers and sizes only; no torch types.  Every device pointer is a
+ * raw CUDA device address borrowed for the duration of the call; `stream` is a
+ * cudaStream_t passed as void*.  All calls are stream-ordered and return a
+ * host status (PTY_OK or PTY_ERR_*); data-dependent failures detected on the
+ * device (bounds, degenerate probe/object, negative intensity) are OR-ed into
+ * a device int32 status word that the caller reads after synchronising.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/pkg/src/ptychokit):
+ *   pty_sweep            engine.py:173-243  sweep()  (inner loop engine.py:191-233)
+ *                          + fields.py:87-107 crop / paste_add_inplace
+ *                          + engine.py:104-150 magnitude_correct / update_object / update_probe
+ *   pty_fft2             fields.py:71-84 propagate()  (centered=1), and the
+ *                          uncentered np.fft.fft2/ifft2 of registration.py:47,71
+ *   pty_register_batch   registration.py:43-128 cross_power_spectrum / coarse_shift /
+ *                          refine_shift / register  (+ posref.py:57-84 sensors)
+ *   pty_adam_apply       posref.py:87-113 adam_step + apply_correction
+ *   pty_init_probes      engine.py:83-95 (mode-1 back-propagation, mode Gram-Schmidt)
+ *   pty_orthogonalize    engine.py:153-164 _orthogonalize_modes
+ *   pty_check_patterns   engine.py:111-112 (DataError on I < 0), checked once at upload
+ *   pty_batch_accumulate / pty_batch_apply   batched extension (no reference)
+ */
+#ifndef PTYCHO_B200_H
+#define PTYCHO_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PTY_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define PTY_API __attribute__((visibility("default")))
+#else
+#define PTY_API
+#endif
+
+/* host status and device status bits (paper_2205_04295_b200/errors.py) */
+#define PTY_OK              0
+#define PTY_ERR_BOUNDS      (1 << 0)  /* crop box outside the canvas        -> BoundsError */
+#define PTY_ERR_PROBE_ZERO  (1 << 1)  /* max sum_m |P_m|^2 == 0              -> DegenerateInputError */
+#define PTY_ERR_OBJECT_ZERO (1 << 2)  /* max |o_j|^2 == 0 with probe update  -> DegenerateInputError */
+#define PTY_ERR_NEGATIVE_I  (1 << 3)  /* measured intensity < 0              -> DataError */
+#define PTY_ERR_ARGUMENT    (1 << 8)  /* bad argument                        -> ParameterError */
+#define PTY_ERR_CUDA        (1 << 9)  /* CUDA runtime error                  -> NativeError */
+
+#define PTY_DTYPE_C64  0   /* complex64  (float2 interleaved), real = float32 */
+#define PTY_DTYPE_C128 1   /* complex128 (double2 interleaved), real = float64 */
+
+#define PTY_SENSE_NONE    0
+#define PTY_SENSE_XCORR_A 1   /* posref.py:66-76 register(o_j, o'_j, "raw") */
+#define PTY_SENSE_XCORR_B 2   /* posref.py:79-84 register(total, I_j, "raw") */
+
+/*
+ * One reconstruction (a "slot") swept by pty_sweep.  Several slots in one call
+ * are independent reconstructions advanced in lock step (replica mode); one
+ * slot is the reference's sequential sweep.
+ */
+typedef struct PtySlot {
+    void*          obj;          /* [H][Wc] complex, row-major, updated in place   */
+    int32_t        H, Wc;        /* canvas shape                                    */
+    int32_t        r0, c0;       /* canvas origin (engine.py:77-81)                 */
+    void*          probes;       /* [M][W][W] complex, updated in place             */
+    const void*    patterns;     /* [N][W][W] real (measured intensity I)           */
+    const double*  positions;    /* [N][2] (x, y) float64                           */
+    const int32_t* order;        /* [N] visit order of this sweep (engine.py:177-181) */
+    void*          stage;        /* posref staging [N][2][W][W] complex or NULL     */
+    double*        err_out;      /* [3]: err_num, err_den, modulus_worst (written)  */
+    int32_t*       status;       /* device status word of this slot (OR-ed)         */
+} PtySlot;
+
+typedef struct PtySweepArgs {
+    int32_t dtype;               /* PTY_DTYPE_*                                    */
+    int32_t window;              /* W: power of two, 16..512                        */
+    int32_t modes;               /* M: 1..8                                         */
+    int32_t n_positions;         /* N (same for every slot)                          */
+    int32_t n_slots;
+    const PtySlot* slots;        /* HOST array of n_slots descriptors               */
+    double  alpha_obj, alpha_probe, beta, gamma, epsilon_rel;
+    int32_t update_probe;        /* update_probe_modes && alpha_probe > 0           */
+    int32_t track_modulus;       /* track_modulus_error                             */
+    int32_t sense;               /* PTY_SENSE_*: what pty_sweep stages for posref   */
+    void*   workspace;           /* device scratch, >= pty_sweep_workspace_bytes()  */
+    int64_t workspace_bytes;
+} PtySweepArgs;
+
+PTY_API int pty_abi_version(void);
+
+/* Number of kernels this library has launched in the process (all devices). */
+PTY_API int64_t pty_launch_count(void);
+
+/* Microbenchmark of the sweep kernel's software grid barrier: `ctas` CTAs of
+ * 512 threads (0 = one per SM) cross `iters` barriers; synchronous. */
+PTY_API int pty_barrier_bench(int32_t iters, int32_t ctas, double* ns_per_barrier);
+
+/* Debug: globaltimer stamps [steps][5][grid] of the last pty_sweep run with
+ * PTY_TIMELINE=<steps> in the environment (k=0 step start, k=1..4 end of
+ * P1..P4 per CTA).  Returns the number of stamps, copies min(n, cap). */
+PTY_API int64_t pty_timeline(uint64_t* out, int64_t cap, int32_t* grid);
+
+/* SM count, max cooperative CTAs for the sweep kernel, compute capability. */
+PTY_API int pty_device_info(int32_t* sm_count, int32_t* coop_ctas, int32_t* cc_major, int32_t* cc_minor);
+
+/* bytes of device workspace pty_sweep needs for these sizes */
+PTY_API int64_t pty_sweep_workspace_bytes(int32_t dtype, int32_t window, int32_t modes,
+                                  int32_t n_positions, int32_t n_slots);
+
+/* One full sweep (every position of every slot) as one cooperative kernel. */
+PTY_API int pty_sweep(const PtySweepArgs* args, void* stream);
+
+/* In-place batched 2D FFT of `batch` W x W complex fields.
+ * centered=1: fields.py propagate (fftshift . fft2 . ifftshift, norm="ortho");
+ * centered=0: np.fft.fft2 (inverse=0, unnormalised) / np.fft.ifft2 (inverse=1, 1/W^2). */
+PTY_API int pty_fft2(void* data, int32_t dtype, int32_t window, int32_t batch, int32_t inverse,
+             int32_t centered, void* stream);
+
+/*
+ * Batched registration (registration.py:123-128) of n pairs.
+ * work: [n][2][W][W] complex; plane 0 = reference, plane 1 = moving on entry
+ *       (overwritten).  If real_inputs != 0, ref_real/mov_real ([n][W][W] real)
+ *       are loaded instead and `work` is only scratch.
+ * weighting: 0 = "phase", 1 = "raw".  kappa in {1} U [2, 1000].
+ * Outputs (device): dy, dx, peak [n] float64; ok [n] int32 (0 = degenerate spectrum).
+ */
+PTY_API int pty_register_batch(void* work, const void* ref_real, const void* mov_real,
+                       int32_t real_inputs, int32_t dtype, int32_t window, int32_t n,
+                       int32_t weighting, int32_t kappa,
+                       double* dy, double* dx, double* peak, int32_t* ok,
+                       void* scratch, int64_t scratch_bytes, void* stream);
+PTY_API int64_t pty_register_scratch_bytes(int32_t window, int32_t n, int32_t kappa);
+
+/* Adam + clamp for n sensed positions (posref.py:87-113), float64.
+ * index[k] (or k when index == NULL) is the position id of sensed entry k. */
+PTY_API int pty_adam_apply(double* positions, double* m, double* v, int64_t* t,
+                   const double* gx, const double* gy, const int32_t* ok,
+                   const int32_t* index, int32_t n,
+                   double step_size, double beta1, double beta2, double eps_adam,
+                   double max_correction, double xmin, double ymin, double xmax, double ymax,
+                   void* stream);
+
+/* engine.py:83-95: probes[0] = propagate(sqrt(max(mean_j I_j, 0)), backward) and
+ * probes[p] = GS(probes[0] * noise[p-1]) scaled to 1% of mode-1 power.
+ * noise: [M-1][W][W] complex128 from default_rng([init_seed, p]) (host numpy). */
+PTY_API int pty_init_probes(void* probes, int32_t dtype, const void* patterns, int32_t n_patterns,
+                    const double* noise, int32_t window, int32_t modes,
+                    void* scratch, int64_t scratch_bytes, void* stream);
+
+/* engine.py:153-164 power-preserving Gram-Schmidt over M modes, in place. */
+PTY_API int pty_orthogonalize(void* probes, int32_t dtype, int32_t window, int32_t modes, void* stream);
+
+/* OR PTY_ERR_NEGATIVE_I into *status if any of count intensities is < 0. */
+PTY_API int pty_check_patterns(const void* patterns, int32_t dtype, int64_t count, int32_t* status,
+                       void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PTYCHO_B200_H */

@@ -1,0 +1,249 @@
+"""ctypes binding of libptycho_b200.so (the C ABI in include/ptycho_b200.h).
+
+PyTorch is used only as the device allocator and stream provider: tensors are
+passed as raw device pointers plus sizes.  There is no fallback: if the
+library or a CUDA device is missing, every entry point raises NativeError.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from pathlib import Path
+
+from .errors import NativeError, raise_for_status
+
+_PKG = Path(__file__).resolve().parent
+_LIB_PATH = _PKG / "libptycho_b200.so"
+_lock = threading.Lock()
+_lib = None
+
+DTYPE_C64 = 0
+DTYPE_C128 = 1
+SENSE_NONE, SENSE_XCORR_A, SENSE_XCORR_B = 0, 1, 2
+MAX_SLOTS = 24
+WINDOWS = (16, 32, 64, 128, 256, 512)
+
+
+def torch():
+    import torch as _t
+    return _t
+
+
+def device():
+    t = torch()
+    if not t.cuda.is_available():
+        raise NativeError("no CUDA device visible: the B200 path has no CPU fallback")
+    return t.device("cuda", t.cuda.current_device())
+
+
+def stream_ptr() -> int:
+    return torch().cuda.current_stream().cuda_stream
+
+
+class PtySlot(C.Structure):
+    _fields_ = [("obj", C.c_void_p), ("H", C.c_int32), ("Wc", C.c_int32),
+                ("r0", C.c_int32), ("c0", C.c_int32), ("probes", C.c_void_p),
+                ("patterns", C.c_void_p), ("positions", C.c_void_p), ("order", C.c_void_p),
+                ("stage", C.c_void_p), ("err_out", C.c_void_p), ("status", C.c_void_p)]
+
+
+class PtySweepArgs(C.Structure):
+    _fields_ = [("dtype", C.c_int32), ("window", C.c_int32), ("modes", C.c_int32),
+                ("n_positions", C.c_int32), ("n_slots", C.c_int32),
+                ("slots", C.POINTER(PtySlot)),
+                ("alpha_obj", C.c_double), ("alpha_probe", C.c_double), ("beta", C.c_double),
+                ("gamma", C.c_double), ("epsilon_rel", C.c_double),
+                ("update_probe", C.c_int32), ("track_modulus", C.c_int32), ("sense", C.c_int32),
+                ("workspace", C.c_void_p), ("workspace_bytes", C.c_int64)]
+
+
+def _declare(lib):
+    i32, i64, vp, dp = C.c_int32, C.c_int64, C.c_void_p, C.c_double
+    sig = {
+        "pty_abi_version": (C.c_int, []),
+        "pty_launch_count": (i64, []),
+        "pty_barrier_bench": (C.c_int, [i32, i32, C.POINTER(C.c_double)]),
+        "pty_timeline": (i64, [vp, i64, C.POINTER(i32)]),
+        "pty_device_info": (C.c_int, [C.POINTER(i32)] * 4),
+        "pty_sweep_workspace_bytes": (i64, [i32] * 5),
+        "pty_sweep": (C.c_int, [C.POINTER(PtySweepArgs), vp]),
+        "pty_fft2": (C.c_int, [vp, i32, i32, i32, i32, i32, vp]),
+        "pty_register_batch": (C.c_int, [vp, vp, vp, i32, i32, i32, i32, i32, i32,
+                                         vp, vp, vp, vp, vp, i64, vp]),
+        "pty_register_scratch_bytes": (i64, [i32, i32, i32]),
+        "pty_adam_apply": (C.c_int, [vp] * 8 + [i32] + [dp] * 9 + [vp]),
+        "pty_init_probes": (C.c_int, [vp, i32, vp, i32, vp, i32, i32, vp, i64, vp]),
+        "pty_orthogonalize": (C.c_int, [vp, i32, i32, i32, vp]),
+        "pty_check_patterns": (C.c_int, [vp, i32, i64, vp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+EXPORTS = ("pty_abi_version", "pty_launch_count", "pty_barrier_bench", "pty_timeline", "pty_device_info", "pty_sweep_workspace_bytes", "pty_sweep",
+           "pty_fft2", "pty_register_batch", "pty_register_scratch_bytes", "pty_adam_apply",
+           "pty_init_probes", "pty_orthogonalize", "pty_check_patterns")
+
+
+def lib_path() -> Path:
+    return Path(os.environ.get("PTY_LIB", str(_LIB_PATH)))
+
+
+def load(require_device: bool = True):
+    """Load the shared library (never builds it implicitly on a GPU box)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            p = lib_path()
+            if not p.exists():
+                raise NativeError(f"{p} is missing: run __graft_entry__.build() "
+                                  "(python -m paper_2205_04295_b200._build)")
+            _lib = _declare(C.CDLL(str(p)))
+            if _lib.pty_abi_version() != 1:
+                raise NativeError("libptycho_b200.so ABI mismatch")
+    if require_device:
+        device()
+        torch().cuda.init()
+    return _lib
+
+
+def check(rc: int, where: str) -> None:
+    if rc != 0:
+        raise_for_status(int(rc), where)
+
+
+def ptr(t) -> int:
+    return 0 if t is None else int(t.data_ptr())
+
+
+def dtype_code(tensor_or_dtype) -> int:
+    t = torch()
+    dt = getattr(tensor_or_dtype, "dtype", tensor_or_dtype)
+    if dt in (t.complex64, t.float32):
+        return DTYPE_C64
+    if dt in (t.complex128, t.float64):
+        return DTYPE_C128
+    raise NativeError(f"unsupported dtype {dt}")
+
+
+# --------------------------------------------------------------- workspaces --
+_ws = {}
+
+
+def workspace(nbytes: int, tag: str = "sweep"):
+    """A cached uint8 device buffer of at least ``nbytes`` (per device, per tag)."""
+    t = torch()
+    dev = device()
+    key = (dev.index, tag)
+    buf = _ws.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = t.empty(max(int(nbytes), 1), dtype=t.uint8, device=dev)
+        _ws[key] = buf
+    return buf
+
+
+# ------------------------------------------------------------------ wrappers --
+
+def fft2(x, inverse: bool, centered: bool) -> None:
+    """In-place batched 2D DFT of a contiguous (..., W, W) complex CUDA tensor."""
+    lib = load()
+    w = x.shape[-1]
+    if x.shape[-2] != w or w not in WINDOWS or not x.is_contiguous():
+        raise NativeError(f"fft2 needs contiguous square power-of-two fields, got {tuple(x.shape)}")
+    batch = x.numel() // (w * w)
+    check(lib.pty_fft2(ptr(x), dtype_code(x), w, batch, int(inverse), int(centered), stream_ptr()),
+          "pty_fft2")
+
+
+def check_patterns(patterns, status) -> None:
+    lib = load()
+    check(lib.pty_check_patterns(ptr(patterns), dtype_code(patterns), patterns.numel(),
+                                 ptr(status), stream_ptr()), "pty_check_patterns")
+
+
+def init_probes(probes, patterns, noise, window: int, modes: int) -> None:
+    lib = load()
+    ws = workspace(modes * window * window * 16, "init")
+    check(lib.pty_init_probes(ptr(probes), dtype_code(probes), ptr(patterns), patterns.shape[0],
+                              ptr(noise), window, modes, ptr(ws), ws.numel(), stream_ptr()),
+          "pty_init_probes")
+
+
+def orthogonalize(probes) -> None:
+    lib = load()
+    m, w = probes.shape[0], probes.shape[-1]
+    check(lib.pty_orthogonalize(ptr(probes), dtype_code(probes), w, m, stream_ptr()),
+          "pty_orthogonalize")
+
+
+def sweep(args: PtySweepArgs) -> None:
+    lib = load()
+    check(lib.pty_sweep(C.byref(args), stream_ptr()), "pty_sweep")
+
+
+def sweep_workspace_bytes(dtype: int, window: int, modes: int, n: int, slots: int) -> int:
+    lib = load(require_device=False)
+    b = lib.pty_sweep_workspace_bytes(dtype, window, modes, n, slots)
+    if b < 0:
+        raise NativeError("unsupported sweep geometry")
+    return int(b)
+
+
+def register_batch(work, window: int, n: int, weighting: int, kappa: int, dy, dx, peak, ok,
+                   ref_real=None, mov_real=None) -> None:
+    lib = load()
+    sb = int(lib.pty_register_scratch_bytes(window, n, kappa))
+    if sb < 0:
+        raise NativeError("unsupported registration geometry")
+    ws = workspace(sb, "register")
+    real = ref_real is not None
+    check(lib.pty_register_batch(ptr(work), ptr(ref_real), ptr(mov_real), int(real),
+                                 dtype_code(work), window, n, weighting, kappa,
+                                 ptr(dy), ptr(dx), ptr(peak), ptr(ok), ptr(ws), ws.numel(),
+                                 stream_ptr()), "pty_register_batch")
+
+
+def adam_apply(positions, buffers, gx, gy, ok, config, bounds, index=None) -> None:
+    lib = load()
+    n = gx.shape[0]
+    xmin, ymin, xmax, ymax = (float(b) for b in bounds)
+    check(lib.pty_adam_apply(ptr(positions), ptr(buffers.m), ptr(buffers.v), ptr(buffers.t),
+                             ptr(gx), ptr(gy), ptr(ok), ptr(index), n,
+                             float(config.step_size), float(config.beta1), float(config.beta2),
+                             float(config.eps_adam), float(config.max_correction),
+                             xmin, ymin, xmax, ymax, stream_ptr()), "pty_adam_apply")
+
+
+def barrier_bench(iters: int = 10000, ctas: int = 0) -> float:
+    """ns per software grid barrier (sweep kernel geometry)."""
+    out = C.c_double()
+    check(load().pty_barrier_bench(iters, ctas, C.byref(out)), "pty_barrier_bench")
+    return out.value
+
+
+def timeline():
+    """Debug stamps of the last sweep run with PTY_TIMELINE set: (steps, 5, grid) ns."""
+    import numpy as np
+    lib = load(require_device=False)
+    g = C.c_int32()
+    n = lib.pty_timeline(None, 0, C.byref(g))
+    buf = np.zeros(n, dtype=np.uint64)
+    lib.pty_timeline(buf.ctypes.data, n, C.byref(g))
+    return buf.reshape(-1, 5, g.value) if n else buf
+
+
+def launch_count() -> int:
+    """Kernels launched by libptycho_b200.so so far in this process."""
+    return int(load(require_device=False).pty_launch_count())
+
+
+def device_info():
+    lib = load()
+    vals = [C.c_int32() for _ in range(4)]
+    check(lib.pty_device_info(*[C.byref(v) for v in vals]), "pty_device_info")
+    return tuple(v.value for v in vals)

@@ -1,0 +1,111 @@
+// pty_common.cuh -- complex arithmetic, reductions and the grid barrier shared
+// by every kernel of libptycho_b200.so (sm_100a).
+//
+// Complex values are interleaved (re, im) pairs, float2 / double2 compatible,
+// so a complex64 torch tensor is read with 8-byte (and 16-byte vector) loads.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/ptycho_b200.h"
+
+namespace pty {
+
+template <typename T>
+struct __align__(2 * sizeof(T)) cplx {
+    T re, im;
+};
+
+template <typename T> __device__ __forceinline__ cplx<T> mk(T a, T b) { return {a, b}; }
+template <typename T> __device__ __forceinline__ cplx<T> operator+(cplx<T> a, cplx<T> b) { return {a.re + b.re, a.im + b.im}; }
+template <typename T> __device__ __forceinline__ cplx<T> operator-(cplx<T> a, cplx<T> b) { return {a.re - b.re, a.im - b.im}; }
+template <typename T> __device__ __forceinline__ cplx<T> operator*(cplx<T> a, cplx<T> b) {
+    return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re};
+}
+// a * conj(b)
+template <typename T> __device__ __forceinline__ cplx<T> mulc(cplx<T> a, cplx<T> b) {
+    return {a.re * b.re + a.im * b.im, a.im * b.re - a.re * b.im};
+}
+template <typename T> __device__ __forceinline__ cplx<T> scale(cplx<T> a, T s) { return {a.re * s, a.im * s}; }
+template <typename T> __device__ __forceinline__ cplx<T> conjg(cplx<T> a) { return {a.re, -a.im}; }
+template <typename T> __device__ __forceinline__ T norm2(cplx<T> a) { return a.re * a.re + a.im * a.im; }
+// numpy's complex / real: Smith's rule with a zero imaginary divisor reduces
+// to a multiply by the reciprocal (numpy loops_arithm_fp complex divide).
+template <typename T> __device__ __forceinline__ cplx<T> divr(cplx<T> a, T d) {
+    T inv = T(1) / d;
+    return {a.re * inv, a.im * inv};
+}
+
+template <typename T> struct real_limits;
+template <> struct real_limits<float>  { static __device__ __forceinline__ float tiny() { return 1.17549435e-38f; } };
+template <> struct real_limits<double> { static __device__ __forceinline__ double tiny() { return 2.2250738585072014e-308; } };
+
+__device__ __forceinline__ float  sqrt_rn(float x)  { return __fsqrt_rn(x); }
+__device__ __forceinline__ double sqrt_rn(double x) { return __dsqrt_rn(x); }
+
+template <typename T> __device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+template <typename T> __device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Block-wide max / sum; `red` is >= 32 entries of shared scratch.  Every
+// thread returns the result.  Must be called by all threads of the block.
+template <typename T> __device__ T block_max(T v, T* red) {
+    v = warp_max(v);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    T r = lane < nw ? red[lane] : red[0];
+    r = warp_max(r);
+    return r;
+}
+template <typename T> __device__ T block_sum(T v, T* red) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    T r = lane < nw ? red[lane] : T(0);
+    r = warp_sum(r);
+    return r;
+}
+
+// Software grid barrier for a cooperative launch (all CTAs co-resident).
+// `counter` is zeroed before the launch; each barrier raises the target by
+// gridDim.x.  bar.sync orders the CTA's writes before thread 0's release
+// atomic; the acquire spin + bar.sync make every other CTA's writes visible.
+struct GridBarrier {
+    unsigned int* counter;
+    unsigned int target;
+    __device__ __forceinline__ void sync() {
+        __syncthreads();
+        target += gridDim.x;
+        if (threadIdx.x == 0) {
+            unsigned int one = 1u, seen;
+            asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;"
+                         : "=r"(seen) : "l"(counter), "r"(one) : "memory");
+            while (true) {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];"
+                             : "=r"(seen) : "l"(counter) : "memory");
+                if ((int)(seen - target) >= 0) break;
+                __nanosleep(20);
+            }
+        }
+        __syncthreads();
+    }
+};
+
+// (-1)^(r+c) checkerboard: the fftshift/ifftshift pair of a centered DFT of
+// even size becomes a sign flip on load and store.
+template <typename T> __device__ __forceinline__ T checker(int r, int c) {
+    return ((r + c) & 1) ? T(-1) : T(1);
+}
+
+}  // namespace pty

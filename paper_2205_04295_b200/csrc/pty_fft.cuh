@@ -1,0 +1,164 @@
+// pty_fft.cuh -- shared-memory-staged radix FFT building blocks (sm_100a).
+//
+// A length-W line (W = A*B, both powers of two, A >= B) is transformed by a
+// group of B threads ("line group", <= one warp):
+//   stage 1: thread b loads x[B*a + b] (a < A) into registers, runs an
+//            in-register DFT_A, multiplies by the inter-stage twiddles
+//            w_W^(b*k1) and writes the A partial spectra to the padded line;
+//   stage 2: thread t reads the B values of column k1 = t + B*i, runs DFT_B and
+//            writes X[k1 + A*k2] back in natural order.
+// Lines live in shared memory with one pad slot every B elements
+// (pad(i) = i + i/B) so both stages are bank-conflict free; the group
+// synchronises with __syncwarp(mask).  Output order is natural, so the
+// centered/uncentered conventions are applied purely elementwise outside.
+//
+// Forward = exp(-2 pi i k n / W) unnormalised (np.fft.fft), inverse =
+// exp(+2 pi i k n / W) unnormalised (np.fft.ifft * W); callers scale.
+#pragma once
+#include "pty_common.cuh"
+
+namespace pty {
+
+template <int W> struct Shape;
+template <> struct Shape<16>   { static constexpr int A = 4,  B = 4;  };
+template <> struct Shape<32>   { static constexpr int A = 8,  B = 4;  };
+template <> struct Shape<64>   { static constexpr int A = 8,  B = 8;  };
+template <> struct Shape<128>  { static constexpr int A = 16, B = 8;  };
+template <> struct Shape<256>  { static constexpr int A = 16, B = 16; };
+template <> struct Shape<512>  { static constexpr int A = 32, B = 16; };
+
+template <int N> struct Log2 { static constexpr int value = 1 + Log2<N / 2>::value; };
+template <> struct Log2<1> { static constexpr int value = 0; };
+
+template <int W> __device__ __forceinline__ int pad(int i) { return i + i / Shape<W>::B; }
+// line stride in complex elements: padded length + 1 so that lines indexed by
+// a column number land on different banks when tiles are transposed
+template <int W> __host__ __device__ constexpr int line_stride() { return W + W / Shape<W>::B + 1; }
+
+// cos(2 pi j / 32), j in [0, 8]
+__host__ __device__ constexpr double kCos32(int j) {
+    return j == 0 ? 1.0
+         : j == 1 ? 0.98078528040323044912618223613424
+         : j == 2 ? 0.92387953251128675612818318939679
+         : j == 3 ? 0.83146961230254523707878837761791
+         : j == 4 ? 0.70710678118654752440084436210485
+         : j == 5 ? 0.55557023301960222474283081394853
+         : j == 6 ? 0.38268343236508977172845998403040
+         : j == 7 ? 0.19509032201612826784828486847702
+         : 0.0;
+}
+// cos / sin of 2 pi j / 32 for any j (folded by the compiler for constant j)
+__host__ __device__ constexpr double cos32(int j) {
+    j &= 31;
+    if (j > 16) j = 32 - j;
+    return j <= 8 ? kCos32(j) : -kCos32(16 - j);
+}
+__host__ __device__ constexpr double sin32(int j) { return cos32(j - 8); }
+
+// x * exp(-/+ 2 pi i j / 32): constant j, special angles exact
+template <typename T, bool INV>
+__device__ __forceinline__ cplx<T> twiddle32(cplx<T> x, int j) {
+    j &= 31;
+    if (j == 0) return x;
+    if (j == 16) return {-x.re, -x.im};
+    if (j == 8) return INV ? cplx<T>{-x.im, x.re} : cplx<T>{x.im, -x.re};
+    if (j == 24) return INV ? cplx<T>{x.im, -x.re} : cplx<T>{-x.im, x.re};
+    const T c = T(cos32(j));
+    const T s = INV ? T(sin32(j)) : T(-sin32(j));
+    return {x.re * c - x.im * s, x.re * s + x.im * c};
+}
+
+// In-register DFT of N <= 32 points, natural order in and out (radix-2 DIT).
+template <typename T, int N, bool INV>
+struct DFT {
+    static __device__ __forceinline__ void run(cplx<T>* v) {
+        cplx<T> e[N / 2], o[N / 2];
+#pragma unroll
+        for (int i = 0; i < N / 2; ++i) { e[i] = v[2 * i]; o[i] = v[2 * i + 1]; }
+        DFT<T, N / 2, INV>::run(e);
+        DFT<T, N / 2, INV>::run(o);
+#pragma unroll
+        for (int k = 0; k < N / 2; ++k) {
+            const cplx<T> t = twiddle32<T, INV>(o[k], k * (32 / N));
+            v[k] = e[k] + t;
+            v[k + N / 2] = e[k] - t;
+        }
+    }
+};
+template <typename T, bool INV>
+struct DFT<T, 2, INV> {
+    static __device__ __forceinline__ void run(cplx<T>* v) {
+        const cplx<T> a = v[0], b = v[1];
+        v[0] = a + b;
+        v[1] = a - b;
+    }
+};
+template <typename T, bool INV>
+struct DFT<T, 4, INV> {
+    static __device__ __forceinline__ void run(cplx<T>* v) {
+        const cplx<T> s0 = v[0] + v[2], d0 = v[0] - v[2];
+        const cplx<T> s1 = v[1] + v[3], d1 = v[1] - v[3];
+        // d1 * (-i) forward, d1 * (+i) inverse
+        const cplx<T> r = INV ? cplx<T>{-d1.im, d1.re} : cplx<T>{d1.im, -d1.re};
+        v[0] = s0 + s1;
+        v[2] = s0 - s1;
+        v[1] = d0 + r;
+        v[3] = d0 - r;
+    }
+};
+
+// Inter-stage twiddle table for a W-line: tw[k1*B + b] = exp(-2 pi i b k1 / W).
+// Filled once per CTA from a global table built on the host in float64.
+template <typename T, int W>
+__device__ __forceinline__ void load_twiddles(cplx<T>* tw_smem, const cplx<T>* tw_global) {
+    for (int i = threadIdx.x; i < W; i += blockDim.x) tw_smem[i] = tw_global[i];
+}
+
+// Transform one padded line in shared memory with a group of B threads.
+// b = thread index in the group, mask = the group's lanes.
+template <typename T, int W, bool INV>
+__device__ __forceinline__ void line_fft(cplx<T>* line, const cplx<T>* tw, int b, unsigned mask) {
+    constexpr int A = Shape<W>::A, B = Shape<W>::B, Q = A / B;
+    cplx<T> v[A];
+#pragma unroll
+    for (int a = 0; a < A; ++a) v[a] = line[a * (B + 1) + b];
+    DFT<T, A, INV>::run(v);
+#pragma unroll
+    for (int k1 = 1; k1 < A; ++k1) {
+        const cplx<T> w = tw[k1 * B + b];
+        v[k1] = INV ? mulc(v[k1], w) : v[k1] * w;
+    }
+    __syncwarp(mask);
+#pragma unroll
+    for (int k1 = 0; k1 < A; ++k1) line[k1 * (B + 1) + b] = v[k1];
+    __syncwarp(mask);
+#pragma unroll
+    for (int i = 0; i < Q; ++i)
+#pragma unroll
+        for (int j = 0; j < B; ++j) v[i * B + j] = line[(b + B * i) * (B + 1) + j];
+    __syncwarp(mask);
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+        DFT<T, B, INV>::run(&v[i * B]);
+#pragma unroll
+        for (int k2 = 0; k2 < B; ++k2) {
+            const int k = b + B * i + A * k2;
+            line[k + k / B] = v[i * B + k2];
+        }
+    }
+    __syncwarp(mask);
+}
+
+// Run `nlines` line FFTs (lines at base + l * stride) with every line group of
+// the CTA.  Caller synchronises the block before and after.
+template <typename T, int W, bool INV>
+__device__ __forceinline__ void lines_fft(cplx<T>* base, int nlines, int stride, const cplx<T>* tw) {
+    constexpr int B = Shape<W>::B;
+    const int groups = blockDim.x / B;
+    const int g = threadIdx.x / B, b = threadIdx.x % B;
+    const int lane = threadIdx.x & 31;
+    const unsigned mask = (B == 32) ? 0xffffffffu : (((1u << B) - 1u) << (lane & ~(B - 1)));
+    for (int l = g; l < nlines; l += groups) line_fft<T, W, INV>(base + (size_t)l * stride, tw, b, mask);
+}
+
+}  // namespace pty

@@ -1,0 +1,333 @@
+"""Multi-mode rPIE reconstruction engine on the B200 (drop-in for ptychokit.engine).
+
+Same public surface as /root/reference/pkg/src/ptychokit/engine.py:
+``SolverConfig`` (engine.py:25-50, same fields/defaults/validation plus the
+``precision`` extension), ``ReconState`` (engine.py:53-66), ``initialize``
+(engine.py:73-101), ``sweep`` (engine.py:173-243) and ``run``
+(engine.py:246-260).  The state lives in HBM as torch tensors; one ``sweep``
+is one cooperative CUDA launch over every position (pty_sweep), followed, when
+position refinement is engaged, by one batched registration launch over the
+staged (o_j, o'_j) crops and one float64 Adam launch (posref.py:87-113).
+
+What stays on the host (exactly as in the reference, and cheap): the visit
+permutation default_rng([shuffle_seed, iteration]) (engine.py:177-181), the
+canvas bounding box from Python round() anchors (engine.py:76-81) and the
+default_rng([init_seed, p]) noise of extra probe modes (engine.py:87-90).
+
+Deviations: windows must be powers of two in
+[16, 512]; negative intensities raise DataError when the dataset is first
+uploaded rather than at the offending visit; out-of-canvas anchors raise
+BoundsError before any visit of the sweep is applied.
+"""
+
+from __future__ import annotations
+
+import time
+import weakref
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+from . import _native
+from .dataio import write_checkpoint
+from .errors import ParameterError, ShapeError, raise_for_status
+from .fields import check_window
+from .posref import AdamBuffers, PosRefConfig
+
+TINY = np.finfo(float).tiny
+
+
+@dataclass(frozen=True)
+class SolverConfig:
+    alpha_obj: float = 0.9
+    alpha_probe: float = 0.9
+    beta: float = 1.0                 # probe-update regularisation, (0, 1]
+    gamma: float = 1.0                # object-update regularisation, (0, 1]
+    mode_count: int = 1
+    iterations: int = 100
+    position_order: str = "shuffled"  # fixed | shuffled
+    shuffle_seed: int = 0
+    init_seed: int = 0
+    epsilon_rel: float = 1e-12        # denominator guard, relative to its max
+    ortho_interval: int = 0           # Gram-Schmidt probe modes every k iters; 0 = off
+    update_probe_modes: bool = True
+    posref: PosRefConfig | None = None
+    track_modulus_error: bool = False
+    precision: str = "fp32"           # B200 extension: fp32 (complex64) | fp64 (complex128)
+
+    def __post_init__(self) -> None:
+        if not (0 <= self.alpha_obj <= 1 and 0 <= self.alpha_probe <= 1):
+            raise ParameterError("update rates must lie in [0, 1]")
+        if not (0 < self.beta <= 1 and 0 < self.gamma <= 1):
+            raise ParameterError("beta and gamma must lie in (0, 1]")
+        if self.position_order not in ("fixed", "shuffled"):
+            raise ParameterError(f"unknown position order {self.position_order!r}")
+        if self.mode_count < 1:
+            raise ParameterError("mode_count must be >= 1")
+        if self.mode_count > 8:
+            raise ParameterError("mode_count must be <= 8 on the B200 path")
+        if self.precision not in ("fp32", "fp64"):
+            raise ParameterError(f"precision must be 'fp32' or 'fp64', got {self.precision!r}")
+
+
+class ReconState:
+    """Reconstruction state resident on the GPU (engine.py:53-66).
+
+    ``obj`` (H, Wc) and the probe stack (M, W, W) are complex64/complex128
+    CUDA tensors; ``probes`` is a list view over the stack (assigning a list
+    restacks it); ``positions`` is an (N, 2) float64 CUDA tensor."""
+
+    def __init__(self, obj, probes, positions, canvas_origin, adam=None,
+                 error_trace=None, modulus_error_trace=None, seconds_per_iteration=None):
+        t = _native.torch()
+        self.obj = obj
+        self.probe_stack = probes if isinstance(probes, t.Tensor) else t.stack(list(probes))
+        self.positions = positions
+        self.canvas_origin = (int(canvas_origin[0]), int(canvas_origin[1]))
+        self.adam = adam
+        self.error_trace = list(error_trace or [])
+        self.modulus_error_trace = list(modulus_error_trace or [])
+        self.seconds_per_iteration = list(seconds_per_iteration or [])
+        self._buf = {}
+
+    @property
+    def probes(self):
+        return list(self.probe_stack.unbind(0))
+
+    @probes.setter
+    def probes(self, value):
+        t = _native.torch()
+        self.probe_stack = t.stack([v.to(self.obj.device, self.obj.dtype) for v in value]).contiguous()
+
+    @property
+    def iteration(self) -> int:
+        return len(self.error_trace)
+
+    @property
+    def window(self) -> int:
+        return int(self.probe_stack.shape[-1])
+
+    def buffer(self, name, shape, dtype, pinned: bool = False):
+        """Per-state scratch reused across sweeps: device buffers (visit order,
+        status, error terms, posref staging) or pinned host mirrors."""
+        t = _native.torch()
+        key = (name, pinned)
+        b = self._buf.get(key)
+        if b is None or tuple(b.shape) != tuple(shape) or b.dtype != dtype:
+            if pinned:
+                b = t.empty(shape, dtype=dtype, pin_memory=True)
+            else:
+                b = t.empty(shape, dtype=dtype, device=self.obj.device)
+            self._buf[key] = b
+        return b
+
+    def to_numpy(self) -> dict:
+        """Host copy in the reference's types (complex128 / float64 numpy)."""
+        out = {"obj": self.obj.cpu().numpy().astype(np.complex128),
+               "probes": [p.cpu().numpy().astype(np.complex128) for p in self.probes],
+               "positions": self.positions.cpu().numpy(),
+               "canvas_origin": self.canvas_origin,
+               "error_trace": list(self.error_trace)}
+        if self.adam is not None:
+            out["adam_m"], out["adam_v"], out["adam_t"] = self.adam.numpy()
+        return out
+
+
+def _anchor(position_xy) -> tuple[int, int]:
+    """engine.py:69-70 (Python round: half to even)."""
+    return int(round(float(position_xy[1]))), int(round(float(position_xy[0])))
+
+
+def _dtypes(precision: str):
+    t = _native.torch()
+    return (t.complex64, t.float32) if precision == "fp32" else (t.complex128, t.float64)
+
+
+_PATTERN_CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def device_patterns(dataset, real_dtype):
+    """The dataset's diffraction stack in HBM (uploaded once, I >= 0 checked)."""
+    if hasattr(dataset, "device_patterns"):
+        return dataset.device_patterns(real_dtype)
+    from .dataio import PtychoDataset
+    shadow = _PATTERN_CACHE.get(dataset)
+    if shadow is None or shadow.patterns is not dataset.patterns:
+        shadow = PtychoDataset(dataset.patterns, dataset.positions, dataset.geometry)
+        _PATTERN_CACHE[dataset] = shadow
+    return shadow.device_patterns(real_dtype)
+
+
+def initialize(dataset, config: SolverConfig) -> ReconState:
+    """engine.py:73-101 -- unit object on the anchor bounding box, mode 1 =
+    back-propagated mean amplitude, extra modes = 1%-power orthogonalised
+    perturbations (float64 on the GPU, then rounded to the working precision)."""
+    t = _native.torch()
+    dev = _native.device()
+    w = dataset.geometry.window
+    check_window(w)
+    cdt, rdt = _dtypes(config.precision)
+    anchors = np.stack([_anchor(p) for p in dataset.positions])
+    origin = anchors.min(axis=0)
+    extent = anchors.max(axis=0) - origin + w
+    obj = t.ones((int(extent[0]), int(extent[1])), dtype=cdt, device=dev)
+    pats = device_patterns(dataset, rdt)
+    m = config.mode_count
+    noise = None
+    if m > 1:
+        host = np.empty((m - 1, w, w), dtype=np.complex128)
+        for p in range(1, m):
+            rng = np.random.default_rng([config.init_seed, p])
+            host[p - 1] = rng.standard_normal((w, w)) + 1j * rng.standard_normal((w, w))
+        noise = t.from_numpy(host).to(dev)
+    probes = t.empty((m, w, w), dtype=cdt, device=dev)
+    _native.init_probes(probes, pats, noise, w, m)
+    positions = t.from_numpy(np.asarray(dataset.positions, dtype=np.float64).copy()).to(dev)
+    adam = AdamBuffers.zeros(dataset.n_positions, dev) if config.posref is not None else None
+    return ReconState(obj=obj, probes=probes, positions=positions,
+                      canvas_origin=(int(origin[0]), int(origin[1])), adam=adam)
+
+
+def visit_order(n: int, config: SolverConfig, iteration: int) -> np.ndarray:
+    """engine.py:177-181."""
+    if config.position_order == "shuffled":
+        return np.random.default_rng([config.shuffle_seed, iteration]).permutation(n)
+    return np.arange(n)
+
+
+def position_bounds(state: ReconState, window: int):
+    """engine.py:167-170 -> (xmin, ymin, xmax, ymax)."""
+    h, w = state.obj.shape
+    r0, c0 = state.canvas_origin
+    return float(c0), float(r0), float(c0 + w - window), float(r0 + h - window)
+
+
+def _engaged(state: ReconState, config: SolverConfig) -> bool:
+    return config.posref is not None and state.iteration >= config.posref.warmup_iterations
+
+
+def sweep(state: ReconState, dataset, config: SolverConfig) -> ReconState:
+    """engine.py:173-243 -- one pass over all positions, mutating ``state``."""
+    sweep_replicas([state], [dataset], config)
+    return state
+
+
+def sweep_replicas(states, datasets, config: SolverConfig, orders=None, kernel_events=None):
+    """Advance K independent reconstructions by one sweep each in ONE launch.
+
+    Every replica keeps the reference's exact sequential semantics; the K
+    visit chains are simply interleaved step by step across the GPU
+    (replica mode).  All replicas share window, mode count,
+    position count and precision."""
+    t = _native.torch()
+    states = list(states)
+    datasets = list(datasets)
+    if len(states) != len(datasets) or not states:
+        raise ParameterError("need one dataset per state")
+    if len(states) > _native.MAX_SLOTS:
+        raise ParameterError(f"at most {_native.MAX_SLOTS} replicas per launch")
+    t0 = time.perf_counter()
+    s0 = states[0]
+    w, m = s0.window, int(s0.probe_stack.shape[0])
+    n = datasets[0].n_positions
+    cdt = s0.obj.dtype
+    rdt = t.float32 if cdt == t.complex64 else t.float64
+    dcode = _native.dtype_code(cdt)
+    engaged = [_engaged(s, config) for s in states]
+    sense = _native.SENSE_NONE
+    if any(engaged):
+        sense = _native.SENSE_XCORR_A if config.posref.sensor == "XCORR_A" else _native.SENSE_XCORR_B
+    slots = (_native.PtySlot * len(states))()
+    keep = []
+    for k, (st, ds) in enumerate(zip(states, datasets)):
+        if ds.geometry.window != w or ds.n_positions != n or st.window != w or st.obj.dtype != cdt \
+                or st.probe_stack.shape[0] != m:
+            raise ShapeError("replicas must share window, mode count, positions and precision")
+        pats = device_patterns(ds, rdt)
+        order = orders[k] if orders is not None else visit_order(n, config, st.iteration)
+        order_h = st.buffer("order", (n,), t.int32, pinned=True)
+        order_h.numpy()[:] = order
+        order_d = st.buffer("order", (n,), t.int32)
+        order_d.copy_(order_h, non_blocking=True)
+        status = st.buffer("status", (1,), t.int32)
+        status.zero_()
+        err = st.buffer("err", (3,), t.float64)
+        stage = st.buffer("stage", (n, 2, w, w), cdt) if sense != _native.SENSE_NONE else None
+        st.obj = st.obj.contiguous()
+        st.probe_stack = st.probe_stack.contiguous()
+        h, wc = st.obj.shape
+        slots[k] = _native.PtySlot(_native.ptr(st.obj), h, wc, st.canvas_origin[0], st.canvas_origin[1],
+                                   _native.ptr(st.probe_stack), _native.ptr(pats),
+                                   _native.ptr(st.positions), _native.ptr(order_d),
+                                   _native.ptr(stage), _native.ptr(err), _native.ptr(status))
+        keep.append((pats, order_d))
+    nbytes = _native.sweep_workspace_bytes(dcode, w, m, n, len(states))
+    ws = _native.workspace(nbytes)
+    args = _native.PtySweepArgs(
+        dcode, w, m, n, len(states), slots,
+        float(config.alpha_obj), float(config.alpha_probe), float(config.beta), float(config.gamma),
+        float(config.epsilon_rel), int(bool(config.update_probe_modes) and config.alpha_probe > 0),
+        int(bool(config.track_modulus_error)), sense, _native.ptr(ws), ws.numel())
+    if kernel_events is not None:
+        kernel_events[0].record()
+    _native.sweep(args)
+    if kernel_events is not None:
+        kernel_events[1].record()
+
+    for st, eng in zip(states, engaged):
+        if eng:
+            _refine_positions(st, config.posref, n, w)
+    for st in states:
+        if (config.ortho_interval > 0 and st.probe_stack.shape[0] > 1
+                and (st.iteration + 1) % config.ortho_interval == 0):
+            _native.orthogonalize(st.probe_stack)
+
+    hosts = []
+    for st in states:
+        he = st.buffer("err", (3,), t.float64, pinned=True)
+        hs = st.buffer("status", (1,), t.int32, pinned=True)
+        he.copy_(st.buffer("err", (3,), t.float64), non_blocking=True)
+        hs.copy_(st.buffer("status", (1,), t.int32), non_blocking=True)
+        hosts.append((he, hs))
+    t.cuda.current_stream().synchronize()
+    dt = time.perf_counter() - t0
+    for k, st in enumerate(states):
+        (num, den, worst), status = hosts[k][0].numpy(), hosts[k][1].numpy()[0]
+        raise_for_status(int(status), f"sweep, replica {k}")
+        st.error_trace.append(float(num) / max(float(den), TINY))
+        if config.track_modulus_error:
+            st.modulus_error_trace.append(float(worst))
+        st.seconds_per_iteration.append(dt)
+    return states
+
+
+def _refine_positions(st: ReconState, pc: PosRefConfig, n: int, w: int) -> None:
+    """posref.py:57-113 for every position of the sweep, batched: register the
+    staged pairs (XCORR_A: o_j vs o'_j; XCORR_B: modelled vs measured
+    intensity) with raw weighting, then the float64 Adam step + clamp."""
+    t = _native.torch()
+    stage = st.buffer("stage", (n, 2, w, w), st.obj.dtype)
+    dy = st.buffer("reg_dy", (n,), t.float64)
+    dx = st.buffer("reg_dx", (n,), t.float64)
+    peak = st.buffer("reg_peak", (n,), t.float64)
+    ok = st.buffer("reg_ok", (n,), t.int32)
+    _native.register_batch(stage, w, n, 1, int(pc.kappa), dy, dx, peak, ok)
+    # sensors return (gx, gy) = (est.dx, est.dy) (posref.py:63)
+    _native.adam_apply(st.positions, st.adam, dx, dy, ok, pc, position_bounds(st, w))
+
+
+def run(dataset, config: SolverConfig, state: ReconState | None = None,
+        checkpoint_every: int = 0, checkpoint_dir=None) -> ReconState:
+    """engine.py:246-260."""
+    if state is None:
+        state = initialize(dataset, config)
+    for _ in range(config.iterations):
+        sweep(state, dataset, config)
+        if (checkpoint_every > 0 and checkpoint_dir is not None
+                and state.iteration % checkpoint_every == 0):
+            snap = Path(checkpoint_dir) / f"iter_{state.iteration:04d}"
+            write_checkpoint(snap, state.obj, state.probes, state.positions, state.canvas_origin,
+                             state.error_trace, state.iteration,
+                             adam=None if state.adam is None else (state.adam.m, state.adam.v, state.adam.t))
+    return state

@@ -1,0 +1,373 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference goldens
+and the CPU oracle, on the same inputs.
+
+Tolerances:
+  fp64 kernels vs reference: relative 1e-9 on fields after short trajectories
+    (ulp-level differences from FMA contraction and FFT rounding, amplified by
+    the iteration), exact on integer outputs;
+  fp32 kernels, one visit / one sweep from the reference state: relative L2
+    <= 1e-5 (object) / 1e-4 (probe) (tier K/S);
+  registration: exact (dy, dx) in fp64, within 1/kappa in fp32.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+import paper_2205_04295_b200 as pk
+from paper_2205_04295_b200 import _native, errors
+from oracle import rpie
+from test_oracle_golden import cfg_from_repr
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_l2(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def make_ds(patterns, positions, window):
+    geom = pk.Geometry.create(8.3187e-10, 0.75, 20e-6, int(window))
+    return pk.PtychoDataset(patterns=np.asarray(patterns, np.float64),
+                            positions=np.asarray(positions, np.float64), geometry=geom)
+
+
+def pkg_cfg(golden_cfg, precision):
+    pr = golden_cfg.posref
+    posref = None
+    if pr is not None:
+        posref = pk.PosRefConfig(sensor=pr.sensor, step_size=pr.step_size, beta1=pr.beta1,
+                                 beta2=pr.beta2, eps_adam=pr.eps_adam,
+                                 warmup_iterations=pr.warmup_iterations, kappa=pr.kappa,
+                                 max_correction=pr.max_correction)
+    keys = ("alpha_obj", "alpha_probe", "beta", "gamma", "mode_count", "position_order",
+            "shuffle_seed", "init_seed", "epsilon_rel", "ortho_interval", "update_probe_modes",
+            "track_modulus_error")
+    return pk.SolverConfig(**{k: getattr(golden_cfg, k) for k in keys}, posref=posref,
+                           precision=precision)
+
+
+# ----------------------------------------------------------------- FFT ----
+
+@pytest.mark.parametrize("w", [16, 32, 64, 128, 256, 512])
+def test_propagate_matches_numpy(gpu, w):
+    rng = np.random.default_rng(w)
+    f = rng.standard_normal((w, w)) + 1j * rng.standard_normal((w, w))
+    want = np.fft.fftshift(np.fft.fft2(np.fft.ifftshift(f), norm="ortho"))
+    got = pk.propagate(f)                         # float64 kernels for numpy input
+    assert np.max(np.abs(got - want)) < 1e-12 * np.max(np.abs(want))
+    back = pk.propagate(got, "backward")
+    assert np.max(np.abs(back - f)) < 1e-12 * np.max(np.abs(f))
+    t = _native.torch()
+    x32 = t.from_numpy(f.astype(np.complex64)).to(gpu)
+    got32 = pk.propagate(x32).cpu().numpy()
+    assert rel_l2(got32, want) < 2e-6
+    e_in = np.sum(np.abs(f) ** 2)
+    assert abs(np.sum(np.abs(got32.astype(np.complex128)) ** 2) - e_in) < 1e-5 * e_in
+
+
+def test_propagate_goldens(gpu):
+    g = golden("fields")
+    for w in (32, 64):
+        np.testing.assert_allclose(pk.propagate(g[f"in_{w}"]), g[f"fwd_{w}"], rtol=0, atol=1e-13)
+        np.testing.assert_allclose(pk.propagate(g[f"in_{w}"], "backward"), g[f"bwd_{w}"],
+                                   rtol=0, atol=1e-13)
+
+
+def test_uncentered_fft_matches_numpy(gpu):
+    t = _native.torch()
+    rng = np.random.default_rng(3)
+    f = rng.standard_normal((4, 64, 64)) + 1j * rng.standard_normal((4, 64, 64))
+    x = t.from_numpy(f).to(gpu)
+    _native.fft2(x, inverse=False, centered=False)
+    np.testing.assert_allclose(x.cpu().numpy(), np.fft.fft2(f), rtol=0, atol=1e-11)
+    _native.fft2(x, inverse=True, centered=False)
+    np.testing.assert_allclose(x.cpu().numpy(), f, rtol=0, atol=1e-13)
+
+
+def test_propagate_rejects_bad_inputs(gpu):
+    with pytest.raises(errors.ShapeError):
+        pk.propagate(np.ones((8, 16), complex))
+    with pytest.raises(ValueError):
+        pk.propagate(np.ones((16, 16), complex), "sideways")
+    with pytest.raises(errors.ShapeError):
+        pk.propagate(np.ones((24, 24), complex))     # not a power of two
+
+
+# ----------------------------------------------------------- one visit ----
+
+def _one_visit_state(o, probes, I, precision):
+    """A canvas equal to the crop and a single position at its origin."""
+    t = _native.torch()
+    cdt = t.complex128 if precision == "fp64" else t.complex64
+    w = o.shape[0]
+    ds = make_ds(I[None], np.zeros((1, 2)), w)
+    st = pk.ReconState(obj=t.from_numpy(o).to("cuda", cdt), probes=t.from_numpy(probes).to("cuda", cdt),
+                       positions=t.zeros((1, 2), dtype=t.float64, device="cuda"), canvas_origin=(0, 0))
+    return st, ds
+
+
+@pytest.mark.parametrize("precision,tol_o,tol_p", [("fp64", 1e-12, 1e-12), ("fp32", 2e-6, 2e-5)])
+def test_single_visit_matches_reference(gpu, precision, tol_o, tol_p):
+    """Tier K: one fused visit vs magnitude_correct + update_object/probe
+    (reference test_engine.py:120-133 at W=64, M=2)."""
+    g = golden("visit")
+    for k in range(4):
+        st, ds = _one_visit_state(g["o"], g["probes"], g["I"], precision)
+        cfg = pk.SolverConfig(alpha_obj=0.9, alpha_probe=0.8, beta=float(g[f"beta_{k}"]),
+                              gamma=float(g[f"gamma_{k}"]), position_order="fixed",
+                              mode_count=2, precision=precision)
+        pk.sweep(st, ds, cfg)
+        assert rel_l2(st.obj.cpu().numpy(), g[f"new_o_{k}"]) < tol_o
+        assert rel_l2(st.probe_stack.cpu().numpy(), g[f"new_p_{k}"]) < tol_p
+
+
+# --------------------------------------------------------- trajectories ----
+
+SWEEP_CASES = ["rpie", "epie_fixed", "ortho_mod", "noprobe", "posref_a", "posref_b"]
+
+
+@pytest.mark.parametrize("name", SWEEP_CASES)
+def test_fp64_trajectory_matches_reference(gpu, name):
+    g = golden(f"sweep_{name}")
+    gcfg = cfg_from_repr(str(g["cfg_repr"]))
+    cfg = pkg_cfg(gcfg, "fp64")
+    ds = make_ds(g["patterns"], g["positions_in"], g["window"])
+    st = pk.initialize(ds, cfg)
+    assert st.canvas_origin == tuple(g["canvas_origin"])
+    np.testing.assert_array_equal(st.obj.cpu().numpy(), g["init_obj"])
+    assert rel_l2(st.probe_stack.cpu().numpy(), g["init_probes"]) < 1e-13
+    for s in range(int(g["sweeps"])):
+        pk.sweep(st, ds, cfg)
+        assert rel_l2(st.obj.cpu().numpy(), g[f"s{s + 1}_obj"]) < 1e-9, s
+        assert rel_l2(st.probe_stack.cpu().numpy(), g[f"s{s + 1}_probes"]) < 1e-9, s
+        np.testing.assert_allclose(st.positions.cpu().numpy(), g[f"s{s + 1}_positions"],
+                                   rtol=0, atol=1e-9)
+        if cfg.posref is not None:
+            m, v, tt = st.adam.numpy()
+            np.testing.assert_array_equal(tt, g[f"s{s + 1}_adam_t"])
+    np.testing.assert_allclose(st.error_trace, g["error_trace"], rtol=1e-9)
+    if cfg.track_modulus_error:
+        assert max(st.modulus_error_trace) <= 1e-9
+
+
+@pytest.mark.parametrize("name", ["rpie", "epie_fixed", "ortho_mod", "posref_a"])
+def test_fp32_sweep_from_reference_state(gpu, name):
+    """Tier S: one fp32 sweep started from the reference's fp64 state."""
+    t = _native.torch()
+    g = golden(f"sweep_{name}")
+    gcfg = cfg_from_repr(str(g["cfg_repr"]))
+    cfg = pkg_cfg(gcfg, "fp32")
+    ds = make_ds(g["patterns"], g["positions_in"], g["window"])
+    for s in range(int(g["sweeps"]) - 1):
+        pre = "init_" if s == 0 else f"s{s}_"
+        st = pk.ReconState(obj=t.from_numpy(g[pre + "obj"]).to("cuda", t.complex64),
+                           probes=t.from_numpy(g[pre + "probes"]).to("cuda", t.complex64),
+                           positions=t.from_numpy(g[pre + "positions"]).to("cuda"),
+                           canvas_origin=tuple(g["canvas_origin"]),
+                           error_trace=list(g["error_trace"][:s]))
+        if cfg.posref is not None:
+            st.adam = pk.AdamBuffers(t.from_numpy(g[pre + "adam_m"]).cuda(),
+                                     t.from_numpy(g[pre + "adam_v"]).cuda(),
+                                     t.from_numpy(g[pre + "adam_t"]).cuda())
+        pk.sweep(st, ds, cfg)
+        assert rel_l2(st.obj.cpu().numpy(), g[f"s{s + 1}_obj"]) < 1e-5, s
+        assert rel_l2(st.probe_stack.cpu().numpy(), g[f"s{s + 1}_probes"]) < 1e-4, s
+        np.testing.assert_allclose(st.positions.cpu().numpy(), g[f"s{s + 1}_positions"],
+                                   rtol=0, atol=1e-3)
+        assert st.error_trace[-1] == pytest.approx(g["error_trace"][s], rel=1e-4)
+
+
+def test_fp64_matches_oracle_at_config1_shape(gpu):
+    """BASELINE configs[0] (10x10 scan, 128^2, M=1, rPIE beta=gamma=0.5).
+
+    Tier T: CUDA fp64 vs the CPU oracle on the same float32 patterns stays
+    <= 1e-6 through 10 iterations.  Beyond that the iteration itself amplifies
+    ulp differences ~10x per sweep (test_chaos_control in test_oracle_cpu.py:
+    the oracle against itself with a 1e-15 probe perturbation reaches 8e-3 by
+    iteration 20), so at 20 iterations parity is tier Q: error trace within 5%.
+    fp32 (tier S): <= 1e-4 (object) / 1e-3 (probe) after 2 iterations."""
+    geom = pk.Geometry.create(8.3187e-10, 0.75, 20e-6, 128)
+    plan = pk.make_scan((10, 10), 16.0, 1.0, seed=1)
+    obj = pk.make_object(pk.canvas_shape_for(plan, 128), "spokes", seed=1)
+    probes = pk.make_probe(pk.ProbeSpec(1, (1.0,), "disk", 30.0), geom)
+    ds = pk.synthesize(obj, probes, plan, geom)
+    ds.patterns = ds.patterns.astype(np.float32).astype(np.float64)   # on-disk precision
+    cfg = pk.SolverConfig(alpha_obj=0.9, alpha_probe=0.9, beta=0.5, gamma=0.5, precision="fp64")
+    st = pk.initialize(ds, cfg)
+    ost = rpie.initialize(ds.patterns, ds.positions, 128, cfg)
+    assert rel_l2(st.probe_stack.cpu().numpy()[0], ost.probes[0]) < 1e-14
+    for it in range(20):
+        pk.sweep(st, ds, cfg)
+        rpie.sweep(ost, ds.patterns, 128, cfg)
+        if it == 9:
+            assert rel_l2(st.obj.cpu().numpy(), ost.obj) < 1e-6
+            assert rel_l2(st.probe_stack.cpu().numpy()[0], ost.probes[0]) < 1e-6
+            np.testing.assert_allclose(st.error_trace, ost.error_trace, rtol=1e-9)
+    np.testing.assert_allclose(st.error_trace, ost.error_trace, rtol=5e-2)
+    ref = golden("simulate")["c1_error_trace"]
+    np.testing.assert_allclose(st.error_trace[:10], ref[:10], rtol=1e-6)
+    np.testing.assert_allclose(st.error_trace, ref, rtol=5e-2)
+    cfg32 = pk.SolverConfig(alpha_obj=0.9, alpha_probe=0.9, beta=0.5, gamma=0.5, precision="fp32")
+    s32 = pk.initialize(ds, cfg32)
+    o64 = rpie.initialize(ds.patterns, ds.positions, 128, cfg32)
+    for _ in range(2):
+        pk.sweep(s32, ds, cfg32)
+        rpie.sweep(o64, ds.patterns, 128, cfg32)
+    assert rel_l2(s32.obj.cpu().numpy(), o64.obj) < 1e-4
+    assert rel_l2(s32.probe_stack.cpu().numpy(), np.stack(o64.probes)) < 1e-3
+
+
+# ------------------------------------------------------------ registration ----
+
+def test_registration_matches_reference(gpu):
+    g = golden("registration")
+    for pair, weighting, kappa, dy, dx, peak in g["rows"]:
+        k = int(pair)
+        est = pk.register(g[f"ref_{k}"], g[f"mov_{k}"], ["phase", "raw"][int(weighting)], int(kappa))
+        assert (est.dy, est.dx) == (dy, dx), (k, weighting, kappa)
+        assert est.peak_value == pytest.approx(peak, rel=1e-9)
+
+
+def test_registration_fp32_within_one_step(gpu):
+    t = _native.torch()
+    g = golden("registration")
+    for pair, weighting, kappa, dy, dx, _ in g["rows"]:
+        k = int(pair)
+        ref = t.from_numpy(g[f"ref_{k}"].astype(np.complex64)).cuda()
+        mov = t.from_numpy(g[f"mov_{k}"].astype(np.complex64)).cuda()
+        est = pk.register(ref, mov, ["phase", "raw"][int(weighting)], int(kappa))
+        assert abs(est.dy - dy) <= 1.0 / kappa + 1e-12 and abs(est.dx - dx) <= 1.0 / kappa + 1e-12
+
+
+def test_registration_edge_cases(gpu):
+    z = np.zeros((16, 16))
+    with pytest.raises(errors.DegenerateInputError):
+        pk.register(z, z, "raw", 10)
+    with pytest.raises(errors.ParameterError):
+        pk.register(np.ones((16, 16)), np.ones((16, 16)), "hann")
+    with pytest.raises(errors.ParameterError):
+        pk.register(np.ones((16, 16)), np.ones((16, 16)), "phase", 1001)
+    with pytest.raises(errors.ShapeError):
+        pk.register(np.ones((16, 16)), np.ones((32, 32)))
+    # exact tie-break (registration.py:72-80; reference test_registration.py:87-100)
+    corr = np.zeros((16, 16))
+    corr[9, 8] = corr[13, 8] = 1.0
+    f = np.fft.ifft2(np.fft.fft2(np.fft.ifftshift(corr)))
+    # register(ref, mov) with xps = F(ref) conj(F(mov)): use mov = delta at 0
+    ref = np.fft.ifftshift(corr)
+    mov = np.zeros((16, 16))
+    mov[0, 0] = 1.0
+    est = pk.register(ref, mov, "raw", 1)
+    assert (est.dy, est.dx) == (1.0, 0.0)
+    assert f.shape == (16, 16)
+
+
+def test_adam_matches_reference(gpu):
+    t = _native.torch()
+    g = golden("adam")
+    pc = pk.PosRefConfig(step_size=0.3, beta1=0.8, beta2=0.95, max_correction=10)
+    buf = pk.AdamBuffers.zeros(3)
+    pos = t.zeros((3, 2), dtype=t.float64, device="cuda")
+    ok = t.ones(3, dtype=t.int32, device="cuda")
+    total = np.zeros((3, 2))
+    for step in range(g["g"].shape[0]):
+        before = pos.cpu().numpy()
+        gg = t.from_numpy(g["g"][step]).cuda()
+        _native.adam_apply(pos, buf, gg[:, 0].contiguous(), gg[:, 1].contiguous(), ok, pc,
+                           (-1e9, -1e9, 1e9, 1e9))
+        np.testing.assert_allclose(pos.cpu().numpy() - before, g["delta"][step], rtol=1e-12, atol=1e-15)
+    m, v, tt = buf.numpy()
+    np.testing.assert_allclose(m, g["m"], rtol=1e-13)
+    np.testing.assert_array_equal(tt, g["t"])
+    p = t.from_numpy(g["pos_in"].copy()).cuda()
+    b2 = pk.AdamBuffers.zeros(3)
+    # apply_correction through a one-step Adam with step chosen to hit the deltas is
+    # covered by the trajectories; here check the clamp alone via max_correction
+    _native.adam_apply(p, b2, t.tensor([1.0, 1.0, -1.0], dtype=t.float64, device="cuda"),
+                       t.tensor([-1.0, -1.0, 1.0], dtype=t.float64, device="cuda"), ok,
+                       pk.PosRefConfig(step_size=20.0, max_correction=20.0), (0.0, 0.0, 10.0, 10.0))
+    np.testing.assert_allclose(p.cpu().numpy(), [[10.0, 0.0], [10.0, 0.0], [0.0, 10.0]], atol=1e-12)
+    assert total.shape == (3, 2)
+
+
+# ------------------------------------------------------ modes & behaviour ----
+
+def test_replicas_equal_independent_sweeps(gpu):
+    """Replica mode: K reconstructions in one launch == K separate sweeps, bitwise."""
+    g = golden("sweep_rpie")
+    gcfg = cfg_from_repr(str(g["cfg_repr"]))
+    cfg = pkg_cfg(gcfg, "fp32")
+    ds = make_ds(g["patterns"], g["positions_in"], g["window"])
+    seeds = [0, 1, 2]
+    alone = []
+    for sd in seeds:
+        c = pk.SolverConfig(**{**cfg.__dict__, "init_seed": sd})
+        st = pk.initialize(ds, c)
+        for _ in range(2):
+            pk.sweep(st, ds, c)
+        alone.append(st)
+    together = [pk.initialize(ds, pk.SolverConfig(**{**cfg.__dict__, "init_seed": sd})) for sd in seeds]
+    for _ in range(2):
+        pk.sweep_replicas(together, [ds] * 3, cfg)
+    for a, b in zip(alone, together):
+        assert np.array_equal(a.obj.cpu().numpy(), b.obj.cpu().numpy())
+        assert np.array_equal(a.probe_stack.cpu().numpy(), b.probe_stack.cpu().numpy())
+        assert a.error_trace == b.error_trace
+
+
+def test_rerun_is_bit_identical(gpu):
+    g = golden("sweep_posref_a")
+    cfg = pkg_cfg(cfg_from_repr(str(g["cfg_repr"])), "fp32")
+    ds = make_ds(g["patterns"], g["positions_in"], g["window"])
+    runs = []
+    for _ in range(2):
+        st = pk.initialize(ds, cfg)
+        for _ in range(3):
+            pk.sweep(st, ds, cfg)
+        runs.append(st)
+    assert np.array_equal(runs[0].obj.cpu().numpy(), runs[1].obj.cpu().numpy())
+    assert np.array_equal(runs[0].positions.cpu().numpy(), runs[1].positions.cpu().numpy())
+    assert runs[0].error_trace == runs[1].error_trace
+
+
+def test_error_behaviour(gpu):
+    t = _native.torch()
+    g = golden("sweep_rpie")
+    ds = make_ds(g["patterns"], g["positions_in"], g["window"])
+    cfg = pk.SolverConfig(mode_count=2)
+    st = pk.initialize(ds, cfg)
+    st.positions[0, 0] = 1e4                               # anchor leaves the canvas
+    with pytest.raises(errors.BoundsError):
+        pk.sweep(st, ds, cfg)
+    st = pk.initialize(ds, cfg)
+    st.probe_stack.zero_()
+    with pytest.raises(errors.DegenerateInputError):
+        pk.sweep(st, ds, cfg)
+    bad = g["patterns"].astype(np.float64).copy()
+    bad[3, 0, 0] = -1.0
+    with pytest.raises(errors.DataError):
+        pk.initialize(make_ds(bad, g["positions_in"], g["window"]), cfg)
+    st = pk.initialize(ds, cfg)
+    st.obj.zero_()
+    with pytest.raises(errors.DegenerateInputError):
+        pk.sweep(st, ds, cfg)
+    st = pk.initialize(ds, pk.SolverConfig())
+    before = st.positions.clone()
+    for _ in range(2):
+        pk.sweep(st, ds, pk.SolverConfig())
+    assert t.equal(before, st.positions)                  # posref off never moves positions
+
+
+def test_posref_engages_only_after_warmup(gpu):
+    g = golden("sweep_posref_a")
+    cfg = pkg_cfg(cfg_from_repr(str(g["cfg_repr"])), "fp32")
+    ds = make_ds(g["patterns"], g["positions_in"], g["window"])
+    st = pk.initialize(ds, cfg)
+    p0 = st.positions.cpu().numpy()
+    pk.sweep(st, ds, cfg)                                  # iteration 0 < warmup 1
+    assert np.array_equal(p0, st.positions.cpu().numpy())
+    pk.sweep(st, ds, cfg)
+    assert not np.array_equal(p0, st.positions.cpu().numpy())
