@@ -13,11 +13,12 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libptycho_b200.so"
-SOURCES = [CSRC / "pty_capi.cu"]
+SOURCES = sorted(CSRC.glob("*.cu"))
 DEPS = sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "ptycho_b200.h"] + SOURCES
+OBJDIR = PKG / "build"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "--std=c++17", "-shared", "-Xcompiler", "-fPIC",
+FLAGS = ["-O3", "-lineinfo", "--std=c++17", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
          "-I", str(ROOT / "include")]
 
@@ -36,18 +37,34 @@ def needs_build() -> bool:
     return any(p.stat().st_mtime > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
+def _compile(src: Path, verbose: bool):
+    obj = OBJDIR / (src.stem + ".o")
+    cmd = [nvcc(), *ARCH, *FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-c", "-o", str(obj), str(src)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    return src, obj, res
+
+
+def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -> Path:
+    """Compile every csrc/*.cu for sm_100a in parallel and link the C-ABI library."""
+    from concurrent.futures import ThreadPoolExecutor
     if not force and not needs_build():
         return LIB
+    OBJDIR.mkdir(exist_ok=True)
+    jobs = jobs or max(1, min(len(SOURCES), os.cpu_count() or 1))
+    with ThreadPoolExecutor(jobs) as ex:
+        results = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
+    failed = [r for r in results if r[2].returncode != 0]
+    for src, _, res in results:
+        if verbose or res.returncode != 0:
+            sys.stderr.write(f"== {src.name}\n" + res.stdout + res.stderr)
+    if failed:
+        raise RuntimeError(f"nvcc failed for {[f[0].name for f in failed]}")
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), *ARCH, *FLAGS, *(["-Xptxas", "-v"] if verbose else []),
-           "-o", str(tmp), *map(str, SOURCES)]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    link = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *[str(r[1]) for r in results]]
+    res = subprocess.run(link, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError(f"nvcc failed ({res.returncode})")
-    if verbose:
-        sys.stderr.write(res.stderr)
+        raise RuntimeError("nvcc link failed")
     os.replace(tmp, LIB)
     return LIB
 

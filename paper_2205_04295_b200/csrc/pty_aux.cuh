@@ -105,7 +105,7 @@ __device__ inline cplx<double> block_csum(cplx<double> v, double* red) {
 // init = 1: engine.py:87-94 -- mode p := mode0 * noise[p-1], projected against
 //   every previous mode, scaled to 1% of mode-0 power;
 // init = 0: engine.py:153-164 -- power-preserving GS of every mode.
-__global__ void __launch_bounds__(1024) gram_schmidt_kernel(cplx<double>* work, int modes, int WW,
+static __global__ void __launch_bounds__(1024) gram_schmidt_kernel(cplx<double>* work, int modes, int WW,
                                                             const cplx<double>* noise, int init) {
     __shared__ double red[64];
     __shared__ cplx<double> coef;

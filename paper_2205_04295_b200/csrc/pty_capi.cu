@@ -1,7 +1,8 @@
 // pty_capi.cu -- extern "C" entry points of libptycho_b200.so
 // (declared in include/ptycho_b200.h).  Host-side only: argument checks,
-// workspace carving, tile-size choice and dtype/window dispatch onto the
-// sm_100a kernels in pty_sweep.cuh, pty_aux.cuh and pty_register.cuh.
+// workspace carving and dtype/window dispatch onto the sm_100a kernels in
+// pty_sweep.cuh (instantiated in pty_sweep_*.cu), pty_aux.cuh and
+// pty_register.cuh.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -11,224 +12,30 @@
 #include <type_traits>
 #include <vector>
 
-#include "pty_aux.cuh"
 #include "pty_register.cuh"
-#include "pty_sweep.cuh"
+#include "pty_sweep_host.cuh"
+
+namespace pty {
+std::atomic<long long> g_launches{0};
+std::vector<unsigned long long> g_timeline;
+int g_timeline_grid = 0;
+extern template int run_sweep<float, 16>(const PtySweepArgs*, cudaStream_t);
+extern template int run_sweep<float, 32>(const PtySweepArgs*, cudaStream_t);
+extern template int run_sweep<float, 64>(const PtySweepArgs*, cudaStream_t);
+extern template int run_sweep<float, 128>(const PtySweepArgs*, cudaStream_t);
+extern template int run_sweep<float, 256>(const PtySweepArgs*, cudaStream_t);
+extern template int run_sweep<float, 512>(const PtySweepArgs*, cudaStream_t);
+extern template int run_sweep<double, 16>(const PtySweepArgs*, cudaStream_t);
+extern template int run_sweep<double, 32>(const PtySweepArgs*, cudaStream_t);
+extern template int run_sweep<double, 64>(const PtySweepArgs*, cudaStream_t);
+extern template int run_sweep<double, 128>(const PtySweepArgs*, cudaStream_t);
+extern template int run_sweep<double, 256>(const PtySweepArgs*, cudaStream_t);
+extern template int run_sweep<double, 512>(const PtySweepArgs*, cudaStream_t);
+}  // namespace pty
 
 using namespace pty;
 
 namespace {
-
-std::atomic<long long> g_launches{0};
-std::vector<unsigned long long> g_timeline;   // debug: last sweep's phase stamps
-int g_timeline_grid = 0;
-inline void count(int k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
-
-constexpr size_t kAlign = 256;
-inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
-
-struct Carver {
-    char* base;
-    size_t off = 0;
-    explicit Carver(void* b) : base(static_cast<char*>(b)) {}
-    template <typename P> P* take(size_t bytes) {
-        P* p = reinterpret_cast<P*>(base ? base + off : nullptr);
-        off += align_up(bytes);
-        return p;
-    }
-};
-
-inline bool valid_window(int W) { return W == 16 || W == 32 || W == 64 || W == 128 || W == 256 || W == 512; }
-
-// Call f(std::integral_constant<int, W>) for the supported windows.
-template <typename F> int with_window(int W, F&& f) {
-    switch (W) {
-        case 16: return f(std::integral_constant<int, 16>{});
-        case 32: return f(std::integral_constant<int, 32>{});
-        case 64: return f(std::integral_constant<int, 64>{});
-        case 128: return f(std::integral_constant<int, 128>{});
-        case 256: return f(std::integral_constant<int, 256>{});
-        case 512: return f(std::integral_constant<int, 512>{});
-        default: return PTY_ERR_ARGUMENT;
-    }
-}
-template <typename F> int with_dtype(int dtype, F&& f) {
-    if (dtype == PTY_DTYPE_C64) return f(float{});
-    if (dtype == PTY_DTYPE_C128) return f(double{});
-    return PTY_ERR_ARGUMENT;
-}
-
-inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? PTY_OK : PTY_ERR_CUDA; }
-inline int last_status() { return cuda_status(cudaGetLastError()); }
-
-int env_int(const char* name, int dflt) {
-    const char* v = std::getenv(name);
-    return v ? std::atoi(v) : dflt;
-}
-
-inline int pow2_floor(int x) {
-    int p = 1;
-    while (p * 2 <= x) p *= 2;
-    return p;
-}
-
-int sm_count() {
-    int dev = 0, n = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    return n;
-}
-
-size_t max_smem_per_sm() {
-    int dev = 0, n = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-    return (size_t)n;
-}
-
-size_t max_dyn_smem() {
-    int dev = 0, n = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    return (size_t)n;
-}
-
-// ------------------------------------------------------------- twiddles --
-// Twiddle tables live in one static device buffer per (dtype, W), built once.
-template <typename T, int W> const cplx<T>* twiddles(cudaStream_t st) {
-    static cplx<T>* table = nullptr;
-    if (!table) {
-        if (cudaMalloc(&table, W * sizeof(cplx<T>)) != cudaSuccess) return nullptr;
-        twiddle_kernel<T, W><<<(W + 255) / 256, 256, 0, st>>>(table);
-        count();
-    }
-    return table;
-}
-
-// ------------------------------------------------------------- sweep ------
-constexpr int kMinTC = 4;   // column tiles are >= 4 complex (32-byte sectors)
-
-struct SweepLayout {
-    unsigned int* barrier;
-    int* anchors;
-    void* scratch;
-    void* omax;
-    void* peak;
-    void* tmax;
-    double* err_part;
-    size_t bytes;
-};
-
-template <typename T>
-SweepLayout carve_sweep(void* ws, int W, int M, int N, int S) {
-    Carver c(ws);
-    SweepLayout L{};
-    L.barrier = c.take<unsigned int>(sizeof(unsigned int));
-    L.anchors = c.take<int>((size_t)S * N * 2 * sizeof(int));
-    L.scratch = c.take<void>((size_t)S * M * W * W * sizeof(cplx<T>));
-    L.omax = c.take<void>((size_t)S * W * sizeof(T));
-    L.peak = c.take<void>((size_t)2 * S * W * sizeof(T));
-    L.tmax = c.take<void>((size_t)S * W * sizeof(T));
-    L.err_part = c.take<double>((size_t)S * N * (W / kMinTC) * 3 * sizeof(double));
-    L.bytes = c.off;
-    return L;
-}
-
-template <typename T, int W>
-int run_sweep(const PtySweepArgs* a, cudaStream_t st) {
-    const int M = a->modes, N = a->n_positions, S = a->n_slots;
-    SweepLayout L = carve_sweep<T>(a->workspace, W, M, N, S);
-    if (!a->workspace || a->workspace_bytes < (int64_t)L.bytes) return PTY_ERR_ARGUMENT;
-    const cplx<T>* tw = twiddles<T, W>(st);
-    if (!tw) return PTY_ERR_CUDA;
-
-    SweepDev P{};
-    P.W = W; P.M = M; P.N = N; P.nslots = S;
-    P.alpha_o = a->alpha_obj; P.alpha_p = a->alpha_probe; P.beta = a->beta; P.gamma = a->gamma;
-    P.eps_rel = a->epsilon_rel;
-    P.update_probe = a->update_probe; P.track_mod = a->track_modulus; P.sense = a->sense;
-    P.barrier = L.barrier; P.anchors = L.anchors; P.scratch = L.scratch;
-    P.omax_part = L.omax; P.peak_part = L.peak; P.tmax_part = L.tmax;
-    P.err_part = L.err_part; P.twiddles = tw;
-    ErrOut outs{};
-    for (int s = 0; s < S; ++s) {
-        const PtySlot& h = a->slots[s];
-        if (!h.obj || !h.probes || !h.patterns || !h.positions || !h.order || !h.status || !h.err_out)
-            return PTY_ERR_ARGUMENT;
-        if (a->sense != PTY_SENSE_NONE && !h.stage) return PTY_ERR_ARGUMENT;
-        if (h.H < W || h.Wc < W) return PTY_ERR_ARGUMENT;
-        P.slot[s] = SlotDev{h.obj, h.H, h.Wc, h.r0, h.c0, h.probes, h.patterns, h.positions,
-                            h.order, h.stage, h.err_out, h.status};
-        outs.p[s] = h.err_out;
-    }
-
-    // launch geometry: kSweepThreads-thread CTAs, `per_sm` of them per SM
-    // (default 2 so one CTA's loads overlap the other's FFTs), cooperative.
-    // Tiles: the smallest power-of-two rows/columns per item that keep the
-    // item count <= the CTA count (every CTA busy even for one reconstruction),
-    // bounded by the per-CTA shared-memory budget.  PTY_TR / PTY_TC /
-    // PTY_CTAS_PER_SM override (tuning).
-    const int sms = sm_count();
-    int per_sm = std::max(1, env_int("PTY_CTAS_PER_SM", kSweepMinCtasPerSm));
-    const size_t smem_sm = max_smem_per_sm();
-    const size_t fixed = sweep_smem_fixed<T, W>();
-    const size_t budget = std::min(max_dyn_smem(), smem_sm / per_sm - 1024 - 512) - fixed;
-    const int grid = sms * per_sm;
-    constexpr int LS = line_stride<W>();
-    const size_t line_bytes = (size_t)LS * sizeof(cplx<T>);
-    int TR = env_int("PTY_TR", 0);
-    if (TR <= 0) {
-        TR = 1;
-        while (TR < W && (long)S * (W / TR) > grid && (size_t)2 * TR * M * line_bytes <= budget) TR *= 2;
-    }
-    int TC = env_int("PTY_TC", 0);
-    if (TC <= 0) {
-        TC = kMinTC;
-        while (TC < W && (long)S * (W / TC) > grid && (size_t)2 * TC * M * line_bytes <= budget) TC *= 2;
-    }
-    if (TR < 1 || TR > W || (W % TR) || TC < kMinTC || TC > W || (W % TC)) return PTY_ERR_ARGUMENT;
-    const int nRT = W / TR, nCT = W / TC;
-    const int K = (S * nCT + grid - 1) / grid;
-    const size_t tile_bytes = std::max((size_t)TR * M * line_bytes, (size_t)K * M * TC * line_bytes);
-    if (tile_bytes > budget) return PTY_ERR_ARGUMENT;   // too many replicas for the resident column tiles
-    P.TR = TR; P.TC = TC; P.nRT = nRT; P.nCT = nCT; P.K = K;
-    P.lgTR = 0; while ((1 << P.lgTR) < TR) ++P.lgTR;
-    P.lgTC = 0; while ((1 << P.lgTC) < TC) ++P.lgTC;
-    const size_t smem = fixed + tile_bytes;
-
-    auto kern = sweep_kernel<T, W>;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-        return PTY_ERR_CUDA;
-    int fit = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, kern, kSweepThreads, smem) != cudaSuccess || fit < per_sm)
-        return PTY_ERR_CUDA;   // the cooperative grid must be co-resident
-
-    // debug timeline (PTY_TIMELINE=<steps>): per-CTA phase completion stamps
-    const int tl_steps = std::min(env_int("PTY_TIMELINE", 0), N);
-    unsigned long long* tl = nullptr;
-    if (tl_steps > 0) {
-        if (cudaMalloc(&tl, (size_t)tl_steps * 5 * grid * sizeof(unsigned long long)) != cudaSuccess) return PTY_ERR_CUDA;
-        P.timeline = tl;
-        P.timeline_steps = tl_steps;
-    }
-    if (cudaMemsetAsync(L.barrier, 0, sizeof(unsigned int), st) != cudaSuccess) return PTY_ERR_CUDA;
-    if (cudaMemsetAsync(L.err_part, 0, (size_t)S * N * nCT * 3 * sizeof(double), st) != cudaSuccess)
-        return PTY_ERR_CUDA;
-    void* args[] = {&P};
-    cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kSweepThreads), args, smem, st);
-    if (e != cudaSuccess) return PTY_ERR_CUDA;
-    sweep_finalize_kernel<<<S, 32, 0, st>>>(L.err_part, N, nCT, S, outs);
-    count(2);
-    if (tl) {
-        g_timeline.assign((size_t)tl_steps * 5 * grid, 0ull);
-        cudaMemcpyAsync(g_timeline.data(), tl, g_timeline.size() * sizeof(unsigned long long),
-                        cudaMemcpyDeviceToHost, st);
-        cudaStreamSynchronize(st);
-        cudaFree(tl);
-        g_timeline_grid = grid;
-    }
-    return last_status();
-}
 
 __global__ void barrier_bench_kernel(unsigned int* counter, int iters, unsigned long long* ns) {
     GridBarrier bar{counter, 0u};

@@ -120,32 +120,343 @@ __device__ __forceinline__ T cta_max_of(const T* p, int n, T* cell) {
     return v;
 }
 
+// One CTA's view of the sweep: shared-memory carve-up, per-thread constants
+// and the four phases, one method per
+// phase body; they are inlined (non-inlined member calls spill the CTA state
+// to local memory, measured 2x slower).
+template <typename T, int W>
+struct SweepCta {
+    using C = cplx<T>;
+    static constexpr int LS = line_stride<W>();
+    const SweepDev& P;
+    C* tw;
+    T* red;
+    C* tile;
+    int* s_dead;
+    int* s_j;
+    int* s_ar;
+    int* s_ac;
+    T* cellT;
+    C* scratch;
+    T* omax_part;
+    T* peak_part;
+    T* tmax_part;
+    int tid, NT, M, N, S;
+    size_t WW;
+    T invW2, alpha_o, alpha_p, beta, gamma, eps_rel;
+
+    __device__ __forceinline__ void phase1(int step) {
+    // ------------------------------------------------------------ P1 rows
+    for (int item = blockIdx.x; item < S * P.nRT; item += gridDim.x) {
+        const int s = item / P.nRT, rt = item % P.nRT;
+        const SlotDev& sl = P.slot[s];
+        if (s_dead[s]) continue;
+        const int ar = s_ar[s], ac = s_ac[s];
+        const C* obj = reinterpret_cast<const C*>(sl.obj);
+        const C* probes = reinterpret_cast<const C*>(sl.probes);
+        // the pattern rows P3 will read: HBM -> L2 while P1/P2 run
+        prefetch_span(reinterpret_cast<const T*>(sl.patterns) + (size_t)s_j[s] * WW + (size_t)rt * P.TR * W,
+                      (size_t)P.TR * W * sizeof(T), false);
+        T om = T(0);
+        constexpr int U = 8;
+        const int nel = P.TR * M * W;          // element = (row, mode, column)
+        batched<U>(nel, [&](int i0) {
+            C o[U], p[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * NT;
+                if (i < nel) {
+                    const int l = i / W, c = i % W, m = l >> P.lgTR, r = l & (P.TR - 1), rr = rt * P.TR + r;
+                    o[u] = obj[(size_t)(ar + rr) * sl.Wc + ac + c];
+                    p[u] = probes[m * WW + (size_t)rr * W + c];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * NT;
+                if (i < nel) {
+                    const int l = i / W, c = i % W, m = l >> P.lgTR, rr = rt * P.TR + (l & (P.TR - 1));
+                    if (m == 0) om = fmax(om, norm2(o[u]));
+                    tile[(size_t)l * LS + pad<W>(c)] = scale(p[u] * o[u], checker<T>(rr, c));
+                }
+            }
+        });
+        om = block_max(om, red);
+        if (tid == 0) omax_part[(size_t)s * P.nRT + rt] = om;
+        __syncthreads();
+        lines_fft<T, W, false>(tile, P.TR * M, LS, tw);
+        __syncthreads();
+        C* scr = scratch + (size_t)s * M * WW;
+        for (int i = tid; i < P.TR * M * W; i += NT) {   // lines are mode-major: contiguous rows
+            const int l = i / W, c = i % W;
+            scr[(l >> P.lgTR) * WW + (size_t)(rt * P.TR + (l & (P.TR - 1))) * W + c] = tile[(size_t)l * LS + pad<W>(c)];
+        }
+        __syncthreads();
+    }
+    }
+
+    __device__ __forceinline__ void phase2(int step) {
+    // ------------------------------------------------- P2 cols (forward)
+    int held = 0;
+    for (int item = blockIdx.x; item < S * P.nCT; item += gridDim.x, ++held) {
+        const int s = item / P.nCT, ct = item % P.nCT;
+        if (s_dead[s]) continue;
+        C* my = tile + (size_t)held * M * P.TC * LS;
+        const C* scr = scratch + (size_t)s * M * WW;
+        {
+            constexpr int U = 8;
+            const int nel = M * W * P.TC;
+            batched<U>(nel, [&](int i0) {
+                C v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int i = i0 + u * NT;
+                    if (i < nel) {
+                        const int rem = i & ((W << P.lgTC) - 1), m = i >> (P.lgTC + Log2<W>::value);
+                        v[u] = scr[m * WW + (size_t)(rem >> P.lgTC) * W + ct * P.TC + (rem & (P.TC - 1))];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int i = i0 + u * NT;
+                    if (i < nel) {
+                        const int rem = i & ((W << P.lgTC) - 1), m = i >> (P.lgTC + Log2<W>::value);
+                        my[(size_t)((m << P.lgTC) + (rem & (P.TC - 1))) * LS + pad<W>(rem >> P.lgTC)] = v[u];
+                    }
+                }
+            });
+        }
+        __syncthreads();
+        lines_fft<T, W, false>(my, M * P.TC, LS, tw);
+        __syncthreads();
+        T tm = T(0);
+        for (int i = tid; i < W * P.TC; i += NT) {
+            const int cc = i / W, r = i % W;   // W is a compile-time power of two
+            T tot = T(0);
+            for (int m = 0; m < M; ++m) tot += norm2(my[(size_t)(m * P.TC + cc) * LS + pad<W>(r)]) * invW2;
+            tm = fmax(tm, tot);
+        }
+        tm = block_max(tm, red);
+        if (tid == 0) tmax_part[(size_t)s * P.nCT + ct] = tm;
+    }
+    }
+
+    __device__ __forceinline__ void phase3(int step) {
+    // ------------------------------------- P3 modulus + cols (inverse)
+    int held = 0;
+    for (int item = blockIdx.x; item < S * P.nCT; item += gridDim.x, ++held) {
+        const int s = item / P.nCT, ct = item % P.nCT;
+        const SlotDev& sl = P.slot[s];
+        if (s_dead[s]) continue;
+        C* my = tile + (size_t)held * M * P.TC * LS;
+        const int j = s_j[s];
+        const T tmax = cta_max_of(tmax_part + (size_t)s * P.nCT, P.nCT, cellT);
+        const T eps = eps_rel * fmax(tmax, real_limits<T>::tiny());
+        const T* I = reinterpret_cast<const T*>(sl.patterns) + (size_t)j * WW;
+        C* stg = P.sense == PTY_SENSE_XCORR_B ? reinterpret_cast<C*>(sl.stage) + (size_t)j * 2 * WW : nullptr;
+        double enum_ = 0.0, eden = 0.0;
+        T worst = T(0);
+        constexpr int UI = 8;
+        const int npx = W * P.TC;
+        batched<UI>(npx, [&](int i0) {
+          T Ib[UI];
+#pragma unroll
+          for (int u = 0; u < UI; ++u) {
+            const int i = i0 + u * NT;
+            if (i < npx) Ib[u] = I[(size_t)(i >> P.lgTC) * W + ct * P.TC + (i & (P.TC - 1))];
+          }
+#pragma unroll
+          for (int u = 0; u < UI; ++u) {
+            const int i = i0 + u * NT;
+            if (i >= npx) continue;
+            const int r = i >> P.lgTC, cc = i & (P.TC - 1), c = ct * P.TC + cc;
+            T tot = T(0);
+            for (int m = 0; m < M; ++m) tot += norm2(my[(size_t)(m * P.TC + cc) * LS + pad<W>(r)]) * invW2;
+            const T Iv = Ib[u];
+            const T sI = sqrt_rn(Iv);
+            const T sc = sI / sqrt_rn(tot + eps);
+            const T d = sqrt_rn(tot) - sI;
+            enum_ += (double)(d * d);
+            eden += (double)Iv;
+            T after = T(0);
+            for (int m = 0; m < M; ++m) {
+                C& a = my[(size_t)(m * P.TC + cc) * LS + pad<W>(r)];
+                a = scale(a, sc);
+                after += norm2(a) * invW2;
+            }
+            if (P.track_mod && tot > T(1e-3) * tmax) {
+                worst = fmax(worst, fabs(after - Iv) / fmax(Iv, real_limits<T>::tiny()));
+            }
+            if (stg) {
+                stg[(size_t)r * W + c] = C{tot, T(0)};
+                stg[WW + (size_t)r * W + c] = C{Iv, T(0)};
+            }
+          }
+        });
+        __syncthreads();
+        lines_fft<T, W, true>(my, M * P.TC, LS, tw);
+        __syncthreads();
+        enum_ = block_sum(enum_, reinterpret_cast<double*>(red));
+        eden = block_sum(eden, reinterpret_cast<double*>(red));
+        worst = block_max(worst, red);
+        if (tid == 0) {
+            double* e = P.err_part + (((size_t)s * N + step) * P.nCT + ct) * 3;
+            e[0] = enum_;
+            e[1] = eden;
+            e[2] = (double)worst;
+        }
+        C* scr = scratch + (size_t)s * M * WW;
+        for (int i = tid; i < M * W * P.TC; i += NT) {
+            const int rem = i & ((W << P.lgTC) - 1), m = i >> (P.lgTC + Log2<W>::value);
+            const int r = rem >> P.lgTC, cc = rem & (P.TC - 1);
+            scr[m * WW + (size_t)r * W + ct * P.TC + cc] = my[(size_t)((m << P.lgTC) + cc) * LS + pad<W>(r)];
+        }
+        __syncthreads();
+    }
+    }
+
+    __device__ __forceinline__ void phase4(int step) {
+    // ------------------------------------------ P4 rows (inverse) + update
+    for (int item = blockIdx.x; item < S * P.nRT; item += gridDim.x) {
+        const int s = item / P.nRT, rt = item % P.nRT;
+        const SlotDev& sl = P.slot[s];
+        if (s_dead[s]) continue;
+        const int j = s_j[s];
+        const T peak = cta_max_of(peak_part + ((size_t)(step & 1) * S + s) * P.nRT, P.nRT, cellT);
+        const T omax = cta_max_of(omax_part + (size_t)s * P.nRT, P.nRT, cellT);
+        if (peak == T(0)) {                      // engine.py:132-134
+            if (tid == 0) atomicOr(sl.status, PTY_ERR_PROBE_ZERO);
+            continue;
+        }
+        if (P.update_probe && omax == T(0)) {    // engine.py:145-147
+            if (tid == 0) atomicOr(sl.status, PTY_ERR_OBJECT_ZERO);
+            continue;
+        }
+        const int ar = s_ar[s], ac = s_ac[s];
+        {   // obj / probe rows of the update: into L1 while the inverse DFTs run
+            const bool l1 = (size_t)P.TR * (M + 1) * W * sizeof(C) <= 16 * 1024;
+            for (int r = 0; r < P.TR; ++r) {
+                const int rr = rt * P.TR + r;
+                prefetch_span(reinterpret_cast<const C*>(sl.obj) + (size_t)(ar + rr) * sl.Wc + ac, W * sizeof(C), l1);
+                for (int m = 0; m < M; ++m)
+                    prefetch_span(reinterpret_cast<const C*>(sl.probes) + m * WW + (size_t)rr * W, W * sizeof(C), l1);
+            }
+        }
+        const C* scr = scratch + (size_t)s * M * WW;
+        {
+            constexpr int U = 8;
+            const int nel = P.TR * M * W;
+            batched<U>(nel, [&](int i0) {
+                C v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int i = i0 + u * NT;
+                    if (i < nel) {
+                        const int l = i / W, c = i % W;
+                        v[u] = scr[(l >> P.lgTR) * WW + (size_t)(rt * P.TR + (l & (P.TR - 1))) * W + c];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int i = i0 + u * NT;
+                    if (i < nel) tile[(size_t)(i / W) * LS + pad<W>(i % W)] = v[u];
+                }
+            });
+        }
+        __syncthreads();
+        lines_fft<T, W, true>(tile, P.TR * M, LS, tw);
+        __syncthreads();
+        C* obj = reinterpret_cast<C*>(sl.obj);
+        C* probes = reinterpret_cast<C*>(sl.probes);
+        C* stg = P.sense == PTY_SENSE_XCORR_A ? reinterpret_cast<C*>(sl.stage) + (size_t)j * 2 * WW : nullptr;
+        const T dmax_o = gamma * peak + (T(1) - gamma) * peak;   // = max of the object denominator
+        const T dmax_p = beta * omax + (T(1) - beta) * omax;
+        T pk = T(0);
+        for (int i = tid; i < P.TR * W; i += NT) {
+            const int r = i / W, c = i % W, rr = rt * P.TR + r;
+            const size_t oi = (size_t)(ar + rr) * sl.Wc + ac + c;
+            const C o = obj[oi];
+            const T sg = checker<T>(rr, c) * invW2;
+            C numer{T(0), T(0)};
+            T pp = T(0);
+            for (int m = 0; m < M; ++m) {
+                const C pv = probes[m * WW + (size_t)rr * W + c];
+                const C psi = scale(tile[(size_t)((m << P.lgTR) + r) * LS + pad<W>(c)], sg);
+                numer = numer + mulc(psi - pv * o, pv);
+                pp += norm2(pv);
+            }
+            T den = gamma * peak + (T(1) - gamma) * pp;
+            den = den + eps_rel * dmax_o;
+            const C no = o + divr(scale(numer, alpha_o), den);
+            obj[oi] = o + (no - o);                              // paste_add_inplace
+            if (stg) {
+                stg[(size_t)rr * W + c] = o;
+                stg[WW + (size_t)rr * W + c] = no;
+            }
+            if (P.update_probe) {
+                const T op = norm2(o);
+                T dp = beta * omax + (T(1) - beta) * op;
+                dp = dp + eps_rel * dmax_p;
+                T npp = T(0);
+                for (int m = 0; m < M; ++m) {   // pre-update probes and o_j (engine.py:218-223)
+                    const size_t pi = m * WW + (size_t)rr * W + c;
+                    const C pv = probes[pi];
+                    const C psi = scale(tile[(size_t)((m << P.lgTR) + r) * LS + pad<W>(c)], sg);
+                    const C np_ = pv + divr(mulc(scale(psi - pv * o, alpha_p), o), dp);
+                    probes[pi] = np_;
+                    npp += norm2(np_);
+                }
+                pk = fmax(pk, npp);
+            } else {
+                pk = fmax(pk, pp);
+            }
+        }
+        pk = block_max(pk, red);
+        if (tid == 0) peak_part[((size_t)((step + 1) & 1) * S + s) * P.nRT + rt] = pk;
+        __syncthreads();
+    }
+    }
+};
+
 template <typename T, int W>
 __global__ void __launch_bounds__(kSweepThreads, kSweepMinCtasPerSm) sweep_kernel(const __grid_constant__ SweepDev P) {
     using C = cplx<T>;
-    constexpr int LS = line_stride<W>();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // per-step snapshot of every slot: dead flag, position index, anchor
     __shared__ int s_dead[kMaxSlots], s_j[kMaxSlots], s_ar[kMaxSlots], s_ac[kMaxSlots];
     __shared__ double s_cell[2];
-    C* tw = reinterpret_cast<C*>(smem_raw);
-    T* red = reinterpret_cast<T*>(smem_raw + (size_t)W * sizeof(C));
-    C* tile = reinterpret_cast<C*>(smem_raw + sweep_smem_fixed<T, W>());
-
-    const int tid = threadIdx.x, NT = blockDim.x;
-    const int M = P.M, N = P.N, S = P.nslots;
-    const T invW2 = T(1) / (T(W) * T(W));
-    const T alpha_o = T(P.alpha_o), alpha_p = T(P.alpha_p), beta = T(P.beta), gamma = T(P.gamma);
-    const T eps_rel = T(P.eps_rel);
+    SweepCta<T, W> X{P};
+    X.tw = reinterpret_cast<C*>(smem_raw);
+    X.red = reinterpret_cast<T*>(smem_raw + (size_t)W * sizeof(C));
+    X.tile = reinterpret_cast<C*>(smem_raw + sweep_smem_fixed<T, W>());
+    X.s_dead = s_dead;
+    X.s_j = s_j;
+    X.s_ar = s_ar;
+    X.s_ac = s_ac;
+    X.cellT = reinterpret_cast<T*>(s_cell);
+    X.scratch = reinterpret_cast<C*>(P.scratch);
+    X.omax_part = reinterpret_cast<T*>(P.omax_part);
+    X.peak_part = reinterpret_cast<T*>(P.peak_part);
+    X.tmax_part = reinterpret_cast<T*>(P.tmax_part);
+    X.tid = threadIdx.x;
+    X.NT = blockDim.x;
+    X.M = P.M;
+    X.N = P.N;
+    X.S = P.nslots;
+    X.WW = (size_t)W * W;
+    X.invW2 = T(1) / (T(W) * T(W));
+    X.alpha_o = T(P.alpha_o);
+    X.alpha_p = T(P.alpha_p);
+    X.beta = T(P.beta);
+    X.gamma = T(P.gamma);
+    X.eps_rel = T(P.eps_rel);
+    const int tid = threadIdx.x, NT = blockDim.x, M = P.M, N = P.N, S = P.nslots;
+    const size_t WW = (size_t)W * W;
+    T* red = X.red;
+    T* peak_part = X.peak_part;
 
     GridBarrier bar{P.barrier, 0u};
-    load_twiddles<T, W>(tw, reinterpret_cast<const C*>(P.twiddles));
-
-    C* scratch = reinterpret_cast<C*>(P.scratch);
-    T* omax_part = reinterpret_cast<T*>(P.omax_part);
-    T* peak_part = reinterpret_cast<T*>(P.peak_part);
-    T* tmax_part = reinterpret_cast<T*>(P.tmax_part);
-    const size_t WW = (size_t)W * W;
+    load_twiddles<T, W>(X.tw, reinterpret_cast<const C*>(P.twiddles));
 
     // ---- phase 0: anchors (engine.py:69-70, 192-195) + bounds, initial probe peak
     for (int idx = blockIdx.x * NT + tid; idx < S * N; idx += gridDim.x * NT) {
@@ -173,7 +484,6 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMinCtasPerSm) sweep_kerne
     }
     bar.sync();
 
-    T* cellT = reinterpret_cast<T*>(s_cell);
     auto stamp = [&](int step, int k) {
         if (P.timeline && step < P.timeline_steps) {
             __syncthreads();
@@ -191,275 +501,16 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMinCtasPerSm) sweep_kerne
             s_ac[tid] = P.anchors[2 * (tid * N + j) + 1];
         }
         __syncthreads();
-        // ------------------------------------------------------------ P1 rows
-        for (int item = blockIdx.x; item < S * P.nRT; item += gridDim.x) {
-            const int s = item / P.nRT, rt = item % P.nRT;
-            const SlotDev& sl = P.slot[s];
-            if (s_dead[s]) continue;
-            const int ar = s_ar[s], ac = s_ac[s];
-            const C* obj = reinterpret_cast<const C*>(sl.obj);
-            const C* probes = reinterpret_cast<const C*>(sl.probes);
-            // the pattern rows P3 will read: HBM -> L2 while P1/P2 run
-            prefetch_span(reinterpret_cast<const T*>(sl.patterns) + (size_t)s_j[s] * WW + (size_t)rt * P.TR * W,
-                          (size_t)P.TR * W * sizeof(T), false);
-            T om = T(0);
-            constexpr int U = 8;
-            const int nel = P.TR * M * W;          // element = (row, mode, column)
-            batched<U>(nel, [&](int i0) {
-                C o[U], p[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int i = i0 + u * NT;
-                    if (i < nel) {
-                        const int l = i / W, c = i % W, m = l >> P.lgTR, r = l & (P.TR - 1), rr = rt * P.TR + r;
-                        o[u] = obj[(size_t)(ar + rr) * sl.Wc + ac + c];
-                        p[u] = probes[m * WW + (size_t)rr * W + c];
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int i = i0 + u * NT;
-                    if (i < nel) {
-                        const int l = i / W, c = i % W, m = l >> P.lgTR, rr = rt * P.TR + (l & (P.TR - 1));
-                        if (m == 0) om = fmax(om, norm2(o[u]));
-                        tile[(size_t)l * LS + pad<W>(c)] = scale(p[u] * o[u], checker<T>(rr, c));
-                    }
-                }
-            });
-            om = block_max(om, red);
-            if (tid == 0) omax_part[(size_t)s * P.nRT + rt] = om;
-            __syncthreads();
-            lines_fft<T, W, false>(tile, P.TR * M, LS, tw);
-            __syncthreads();
-            C* scr = scratch + (size_t)s * M * WW;
-            for (int i = tid; i < P.TR * M * W; i += NT) {   // lines are mode-major: contiguous rows
-                const int l = i / W, c = i % W;
-                scr[(l >> P.lgTR) * WW + (size_t)(rt * P.TR + (l & (P.TR - 1))) * W + c] = tile[(size_t)l * LS + pad<W>(c)];
-            }
-            __syncthreads();
-        }
+        X.phase1(step);
         stamp(step, 1);
         bar.sync();
-
-        // ------------------------------------------------- P2 cols (forward)
-        int held = 0;
-        for (int item = blockIdx.x; item < S * P.nCT; item += gridDim.x, ++held) {
-            const int s = item / P.nCT, ct = item % P.nCT;
-            if (s_dead[s]) continue;
-            C* my = tile + (size_t)held * M * P.TC * LS;
-            const C* scr = scratch + (size_t)s * M * WW;
-            {
-                constexpr int U = 8;
-                const int nel = M * W * P.TC;
-                batched<U>(nel, [&](int i0) {
-                    C v[U];
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const int i = i0 + u * NT;
-                        if (i < nel) {
-                            const int rem = i & ((W << P.lgTC) - 1), m = i >> (P.lgTC + Log2<W>::value);
-                            v[u] = scr[m * WW + (size_t)(rem >> P.lgTC) * W + ct * P.TC + (rem & (P.TC - 1))];
-                        }
-                    }
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const int i = i0 + u * NT;
-                        if (i < nel) {
-                            const int rem = i & ((W << P.lgTC) - 1), m = i >> (P.lgTC + Log2<W>::value);
-                            my[(size_t)((m << P.lgTC) + (rem & (P.TC - 1))) * LS + pad<W>(rem >> P.lgTC)] = v[u];
-                        }
-                    }
-                });
-            }
-            __syncthreads();
-            lines_fft<T, W, false>(my, M * P.TC, LS, tw);
-            __syncthreads();
-            T tm = T(0);
-            for (int i = tid; i < W * P.TC; i += NT) {
-                const int cc = i / W, r = i % W;   // W is a compile-time power of two
-                T tot = T(0);
-                for (int m = 0; m < M; ++m) tot += norm2(my[(size_t)(m * P.TC + cc) * LS + pad<W>(r)]) * invW2;
-                tm = fmax(tm, tot);
-            }
-            tm = block_max(tm, red);
-            if (tid == 0) tmax_part[(size_t)s * P.nCT + ct] = tm;
-        }
+        X.phase2(step);
         stamp(step, 2);
         bar.sync();
-
-        // ------------------------------------- P3 modulus + cols (inverse)
-        held = 0;
-        for (int item = blockIdx.x; item < S * P.nCT; item += gridDim.x, ++held) {
-            const int s = item / P.nCT, ct = item % P.nCT;
-            const SlotDev& sl = P.slot[s];
-            if (s_dead[s]) continue;
-            C* my = tile + (size_t)held * M * P.TC * LS;
-            const int j = s_j[s];
-            const T tmax = cta_max_of(tmax_part + (size_t)s * P.nCT, P.nCT, cellT);
-            const T eps = eps_rel * fmax(tmax, real_limits<T>::tiny());
-            const T* I = reinterpret_cast<const T*>(sl.patterns) + (size_t)j * WW;
-            C* stg = P.sense == PTY_SENSE_XCORR_B ? reinterpret_cast<C*>(sl.stage) + (size_t)j * 2 * WW : nullptr;
-            double enum_ = 0.0, eden = 0.0;
-            T worst = T(0);
-            constexpr int UI = 8;
-            const int npx = W * P.TC;
-            batched<UI>(npx, [&](int i0) {
-              T Ib[UI];
-#pragma unroll
-              for (int u = 0; u < UI; ++u) {
-                const int i = i0 + u * NT;
-                if (i < npx) Ib[u] = I[(size_t)(i >> P.lgTC) * W + ct * P.TC + (i & (P.TC - 1))];
-              }
-#pragma unroll
-              for (int u = 0; u < UI; ++u) {
-                const int i = i0 + u * NT;
-                if (i >= npx) continue;
-                const int r = i >> P.lgTC, cc = i & (P.TC - 1), c = ct * P.TC + cc;
-                T tot = T(0);
-                for (int m = 0; m < M; ++m) tot += norm2(my[(size_t)(m * P.TC + cc) * LS + pad<W>(r)]) * invW2;
-                const T Iv = Ib[u];
-                const T sI = sqrt_rn(Iv);
-                const T sc = sI / sqrt_rn(tot + eps);
-                const T d = sqrt_rn(tot) - sI;
-                enum_ += (double)(d * d);
-                eden += (double)Iv;
-                T after = T(0);
-                for (int m = 0; m < M; ++m) {
-                    C& a = my[(size_t)(m * P.TC + cc) * LS + pad<W>(r)];
-                    a = scale(a, sc);
-                    after += norm2(a) * invW2;
-                }
-                if (P.track_mod && tot > T(1e-3) * tmax) {
-                    worst = fmax(worst, fabs(after - Iv) / fmax(Iv, real_limits<T>::tiny()));
-                }
-                if (stg) {
-                    stg[(size_t)r * W + c] = C{tot, T(0)};
-                    stg[WW + (size_t)r * W + c] = C{Iv, T(0)};
-                }
-              }
-            });
-            __syncthreads();
-            lines_fft<T, W, true>(my, M * P.TC, LS, tw);
-            __syncthreads();
-            enum_ = block_sum(enum_, reinterpret_cast<double*>(red));
-            eden = block_sum(eden, reinterpret_cast<double*>(red));
-            worst = block_max(worst, red);
-            if (tid == 0) {
-                double* e = P.err_part + (((size_t)s * N + step) * P.nCT + ct) * 3;
-                e[0] = enum_;
-                e[1] = eden;
-                e[2] = (double)worst;
-            }
-            C* scr = scratch + (size_t)s * M * WW;
-            for (int i = tid; i < M * W * P.TC; i += NT) {
-                const int rem = i & ((W << P.lgTC) - 1), m = i >> (P.lgTC + Log2<W>::value);
-                const int r = rem >> P.lgTC, cc = rem & (P.TC - 1);
-                scr[m * WW + (size_t)r * W + ct * P.TC + cc] = my[(size_t)((m << P.lgTC) + cc) * LS + pad<W>(r)];
-            }
-            __syncthreads();
-        }
+        X.phase3(step);
         stamp(step, 3);
         bar.sync();
-
-        // ------------------------------------------ P4 rows (inverse) + update
-        for (int item = blockIdx.x; item < S * P.nRT; item += gridDim.x) {
-            const int s = item / P.nRT, rt = item % P.nRT;
-            const SlotDev& sl = P.slot[s];
-            if (s_dead[s]) continue;
-            const int j = s_j[s];
-            const T peak = cta_max_of(peak_part + ((size_t)(step & 1) * S + s) * P.nRT, P.nRT, cellT);
-            const T omax = cta_max_of(omax_part + (size_t)s * P.nRT, P.nRT, cellT);
-            if (peak == T(0)) {                      // engine.py:132-134
-                if (tid == 0) atomicOr(sl.status, PTY_ERR_PROBE_ZERO);
-                continue;
-            }
-            if (P.update_probe && omax == T(0)) {    // engine.py:145-147
-                if (tid == 0) atomicOr(sl.status, PTY_ERR_OBJECT_ZERO);
-                continue;
-            }
-            const int ar = s_ar[s], ac = s_ac[s];
-            {   // obj / probe rows of the update: into L1 while the inverse DFTs run
-                const bool l1 = (size_t)P.TR * (M + 1) * W * sizeof(C) <= 16 * 1024;
-                for (int r = 0; r < P.TR; ++r) {
-                    const int rr = rt * P.TR + r;
-                    prefetch_span(reinterpret_cast<const C*>(sl.obj) + (size_t)(ar + rr) * sl.Wc + ac, W * sizeof(C), l1);
-                    for (int m = 0; m < M; ++m)
-                        prefetch_span(reinterpret_cast<const C*>(sl.probes) + m * WW + (size_t)rr * W, W * sizeof(C), l1);
-                }
-            }
-            const C* scr = scratch + (size_t)s * M * WW;
-            {
-                constexpr int U = 8;
-                const int nel = P.TR * M * W;
-                batched<U>(nel, [&](int i0) {
-                    C v[U];
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const int i = i0 + u * NT;
-                        if (i < nel) {
-                            const int l = i / W, c = i % W;
-                            v[u] = scr[(l >> P.lgTR) * WW + (size_t)(rt * P.TR + (l & (P.TR - 1))) * W + c];
-                        }
-                    }
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const int i = i0 + u * NT;
-                        if (i < nel) tile[(size_t)(i / W) * LS + pad<W>(i % W)] = v[u];
-                    }
-                });
-            }
-            __syncthreads();
-            lines_fft<T, W, true>(tile, P.TR * M, LS, tw);
-            __syncthreads();
-            C* obj = reinterpret_cast<C*>(sl.obj);
-            C* probes = reinterpret_cast<C*>(sl.probes);
-            C* stg = P.sense == PTY_SENSE_XCORR_A ? reinterpret_cast<C*>(sl.stage) + (size_t)j * 2 * WW : nullptr;
-            const T dmax_o = gamma * peak + (T(1) - gamma) * peak;   // = max of the object denominator
-            const T dmax_p = beta * omax + (T(1) - beta) * omax;
-            T pk = T(0);
-            for (int i = tid; i < P.TR * W; i += NT) {
-                const int r = i / W, c = i % W, rr = rt * P.TR + r;
-                const size_t oi = (size_t)(ar + rr) * sl.Wc + ac + c;
-                const C o = obj[oi];
-                const T sg = checker<T>(rr, c) * invW2;
-                C numer{T(0), T(0)};
-                T pp = T(0);
-                for (int m = 0; m < M; ++m) {
-                    const C pv = probes[m * WW + (size_t)rr * W + c];
-                    const C psi = scale(tile[(size_t)((m << P.lgTR) + r) * LS + pad<W>(c)], sg);
-                    numer = numer + mulc(psi - pv * o, pv);
-                    pp += norm2(pv);
-                }
-                T den = gamma * peak + (T(1) - gamma) * pp;
-                den = den + eps_rel * dmax_o;
-                const C no = o + divr(scale(numer, alpha_o), den);
-                obj[oi] = o + (no - o);                              // paste_add_inplace
-                if (stg) {
-                    stg[(size_t)rr * W + c] = o;
-                    stg[WW + (size_t)rr * W + c] = no;
-                }
-                if (P.update_probe) {
-                    const T op = norm2(o);
-                    T dp = beta * omax + (T(1) - beta) * op;
-                    dp = dp + eps_rel * dmax_p;
-                    T npp = T(0);
-                    for (int m = 0; m < M; ++m) {   // pre-update probes and o_j (engine.py:218-223)
-                        const size_t pi = m * WW + (size_t)rr * W + c;
-                        const C pv = probes[pi];
-                        const C psi = scale(tile[(size_t)((m << P.lgTR) + r) * LS + pad<W>(c)], sg);
-                        const C np_ = pv + divr(mulc(scale(psi - pv * o, alpha_p), o), dp);
-                        probes[pi] = np_;
-                        npp += norm2(np_);
-                    }
-                    pk = fmax(pk, npp);
-                } else {
-                    pk = fmax(pk, pp);
-                }
-            }
-            pk = block_max(pk, red);
-            if (tid == 0) peak_part[((size_t)((step + 1) & 1) * S + s) * P.nRT + rt] = pk;
-            __syncthreads();
-        }
+        X.phase4(step);
         stamp(step, 4);
         bar.sync();
     }
@@ -470,7 +521,7 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMinCtasPerSm) sweep_kerne
 struct ErrOut {
     double* p[kMaxSlots];
 };
-__global__ void sweep_finalize_kernel(const double* err_part, int N, int nCT, int nslots, ErrOut outs) {
+static __global__ void sweep_finalize_kernel(const double* err_part, int N, int nCT, int nslots, ErrOut outs) {
     const int s = blockIdx.x;
     if (s >= nslots || threadIdx.x != 0) return;
     double num = 0.0, den = 0.0, worst = 0.0;

@@ -1,0 +1,5 @@
+// explicit instantiation of the sweep for float, W = 128
+#include "pty_sweep_host.cuh"
+namespace pty {
+template int run_sweep<float, 128>(const PtySweepArgs*, cudaStream_t);
+}

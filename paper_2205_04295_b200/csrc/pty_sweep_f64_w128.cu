@@ -1,0 +1,5 @@
+// explicit instantiation of the sweep for double, W = 128
+#include "pty_sweep_host.cuh"
+namespace pty {
+template int run_sweep<double, 128>(const PtySweepArgs*, cudaStream_t);
+}

@@ -1,0 +1,5 @@
+// explicit instantiation of the sweep for double, W = 64
+#include "pty_sweep_host.cuh"
+namespace pty {
+template int run_sweep<double, 64>(const PtySweepArgs*, cudaStream_t);
+}
