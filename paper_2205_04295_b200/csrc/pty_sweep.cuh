@@ -516,29 +516,34 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMinCtasPerSm) sweep_kerne
     }
 }
 
-// Deterministic end-of-sweep reduction of the per-visit error partials in
-// visit order (engine.py:198-202, 239-241): one thread per slot.
+// Deterministic end-of-sweep reduction of the per-visit error partials
+// (engine.py:198-202, 239-241): one CTA per slot, thread t sums visits
+// t, t+256, ... in order, then a fixed shuffle tree -- same order every run.
 struct ErrOut {
     double* p[kMaxSlots];
 };
-static __global__ void sweep_finalize_kernel(const double* err_part, int N, int nCT, int nslots, ErrOut outs) {
+static __global__ void __launch_bounds__(256) sweep_finalize_kernel(const double* err_part, int N, int nCT,
+                                                                    int nslots, ErrOut outs) {
+    __shared__ double red[32];
     const int s = blockIdx.x;
-    if (s >= nslots || threadIdx.x != 0) return;
+    if (s >= nslots) return;
     double num = 0.0, den = 0.0, worst = 0.0;
-    for (int k = 0; k < N; ++k) {
-        double vn = 0.0, vd = 0.0;
+    for (int k = threadIdx.x; k < N; k += blockDim.x) {
         for (int ct = 0; ct < nCT; ++ct) {
             const double* e = err_part + (((size_t)s * N + k) * nCT + ct) * 3;
-            vn += e[0];
-            vd += e[1];
+            num += e[0];
+            den += e[1];
             worst = fmax(worst, e[2]);
         }
-        num += vn;
-        den += vd;
     }
-    outs.p[s][0] = num;
-    outs.p[s][1] = den;
-    outs.p[s][2] = worst;
+    num = block_sum(num, red);
+    den = block_sum(den, red);
+    worst = block_max(worst, red);
+    if (threadIdx.x == 0) {
+        outs.p[s][0] = num;
+        outs.p[s][1] = den;
+        outs.p[s][2] = worst;
+    }
 }
 
 }  // namespace pty

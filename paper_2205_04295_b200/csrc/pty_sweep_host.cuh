@@ -120,7 +120,7 @@ int run_sweep(const PtySweepArgs* a, cudaStream_t st) {
     void* args[] = {&P};
     cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kSweepThreads), args, smem, st);
     if (e != cudaSuccess) return PTY_ERR_CUDA;
-    sweep_finalize_kernel<<<S, 32, 0, st>>>(L.err_part, N, nCT, S, outs);
+    sweep_finalize_kernel<<<S, 256, 0, st>>>(L.err_part, N, nCT, S, outs);
     count(2);
     if (tl) {
         g_timeline.assign((size_t)tl_steps * 5 * grid, 0ull);
