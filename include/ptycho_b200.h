@@ -20,7 +20,9 @@
  *   pty_init_probes      engine.py:83-95 (mode-1 back-propagation, mode Gram-Schmidt)
  *   pty_orthogonalize    engine.py:153-164 _orthogonalize_modes
  *   pty_check_patterns   engine.py:111-112 (DataError on I < 0), checked once at upload
- *   pty_batch_accumulate / pty_batch_apply   batched extension (no reference)
+ *   pty_batch_contrib / pty_batch_apply / pty_batch_finalize
+ *                        batched (semi-parallel) extension -- no reference
+ *                        counterpart; CPU statement oracle/batched.py
  */
 #ifndef PTYCHO_B200_H
 #define PTYCHO_B200_H
@@ -155,6 +157,44 @@ PTY_API int pty_orthogonalize(void* probes, int32_t dtype, int32_t window, int32
 /* OR PTY_ERR_NEGATIVE_I into *status if any of count intensities is < 0. */
 PTY_API int pty_check_patterns(const void* patterns, int32_t dtype, int64_t count, int32_t* status,
                        void* stream);
+
+/*
+ * Batched (semi-parallel) rPIE, one batch of positions of ONE reconstruction.
+ * pty_batch_contrib computes every position of `batch` against the batch-start
+ * state and leaves the summed update terms in the caller-owned accumulators:
+ *   obj_acc   [3][H][Wc]  real: object numerator (re, im), denominator
+ *   probe_acc [2M+1][W][W] real: probe numerator (re, im) per mode, denominator
+ * (real = float for PTY_DTYPE_C64, double for C128).  Ranks that split a batch
+ * all-reduce (sum) both accumulators, then every rank calls pty_batch_apply.
+ * err_part [n_positions][W/4][3] is indexed by visit rank (visit0 + k) and
+ * reduced once per sweep by pty_batch_finalize (deterministic order).
+ */
+typedef struct PtyBatchArgs {
+    int32_t dtype, window, modes, n_positions;
+    void*   obj;
+    int32_t H, Wc, r0, c0;
+    void*   probes;
+    const void*    patterns;     /* [N][W][W] real                              */
+    const double*  positions;    /* [N][2] (x, y) float64                       */
+    const int32_t* batch;        /* [n_batch] position ids (this rank's slice)  */
+    int32_t n_batch, visit0;
+    double  alpha_obj, alpha_probe, beta, gamma, epsilon_rel;
+    int32_t update_probe, track_modulus, sense;
+    void*   stage;               /* [N][2][W][W] complex posref staging or NULL */
+    void*   obj_acc;
+    void*   probe_acc;
+    double* err_part;
+    int32_t* status;
+    void*   workspace;
+    int64_t workspace_bytes;
+} PtyBatchArgs;
+
+PTY_API int64_t pty_batch_workspace_bytes(int32_t dtype, int32_t window, int32_t modes,
+                                          int32_t n_batch, int32_t H, int32_t Wc);
+PTY_API int pty_batch_contrib(const PtyBatchArgs* args, void* stream);
+PTY_API int pty_batch_apply(const PtyBatchArgs* args, void* stream);
+PTY_API int pty_batch_finalize(const double* err_part, int32_t n_visits, int32_t window,
+                               double* err_out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -59,6 +59,20 @@ class PtySweepArgs(C.Structure):
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_int64)]
 
 
+class PtyBatchArgs(C.Structure):
+    _fields_ = [("dtype", C.c_int32), ("window", C.c_int32), ("modes", C.c_int32),
+                ("n_positions", C.c_int32), ("obj", C.c_void_p), ("H", C.c_int32), ("Wc", C.c_int32),
+                ("r0", C.c_int32), ("c0", C.c_int32), ("probes", C.c_void_p),
+                ("patterns", C.c_void_p), ("positions", C.c_void_p), ("batch", C.c_void_p),
+                ("n_batch", C.c_int32), ("visit0", C.c_int32),
+                ("alpha_obj", C.c_double), ("alpha_probe", C.c_double), ("beta", C.c_double),
+                ("gamma", C.c_double), ("epsilon_rel", C.c_double),
+                ("update_probe", C.c_int32), ("track_modulus", C.c_int32), ("sense", C.c_int32),
+                ("stage", C.c_void_p), ("obj_acc", C.c_void_p), ("probe_acc", C.c_void_p),
+                ("err_part", C.c_void_p), ("status", C.c_void_p),
+                ("workspace", C.c_void_p), ("workspace_bytes", C.c_int64)]
+
+
 def _declare(lib):
     i32, i64, vp, dp = C.c_int32, C.c_int64, C.c_void_p, C.c_double
     sig = {
@@ -77,6 +91,10 @@ def _declare(lib):
         "pty_init_probes": (C.c_int, [vp, i32, vp, i32, vp, i32, i32, vp, i64, vp]),
         "pty_orthogonalize": (C.c_int, [vp, i32, i32, i32, vp]),
         "pty_check_patterns": (C.c_int, [vp, i32, i64, vp, vp]),
+        "pty_batch_workspace_bytes": (i64, [i32] * 6),
+        "pty_batch_contrib": (C.c_int, [C.POINTER(PtyBatchArgs), vp]),
+        "pty_batch_apply": (C.c_int, [C.POINTER(PtyBatchArgs), vp]),
+        "pty_batch_finalize": (C.c_int, [vp, i32, i32, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -87,7 +105,8 @@ def _declare(lib):
 
 EXPORTS = ("pty_abi_version", "pty_launch_count", "pty_barrier_bench", "pty_timeline", "pty_device_info", "pty_sweep_workspace_bytes", "pty_sweep",
            "pty_fft2", "pty_register_batch", "pty_register_scratch_bytes", "pty_adam_apply",
-           "pty_init_probes", "pty_orthogonalize", "pty_check_patterns")
+           "pty_init_probes", "pty_orthogonalize", "pty_check_patterns",
+           "pty_batch_workspace_bytes", "pty_batch_contrib", "pty_batch_apply", "pty_batch_finalize")
 
 
 def lib_path() -> Path:
@@ -240,6 +259,26 @@ def timeline():
 def launch_count() -> int:
     """Kernels launched by libptycho_b200.so so far in this process."""
     return int(load(require_device=False).pty_launch_count())
+
+
+def batch_workspace_bytes(dtype: int, window: int, modes: int, b: int, h: int, wc: int) -> int:
+    b_ = load(require_device=False).pty_batch_workspace_bytes(dtype, window, modes, b, h, wc)
+    if b_ < 0:
+        raise NativeError("unsupported batch geometry")
+    return int(b_)
+
+
+def batch_contrib(args: PtyBatchArgs) -> None:
+    check(load().pty_batch_contrib(C.byref(args), stream_ptr()), "pty_batch_contrib")
+
+
+def batch_apply(args: PtyBatchArgs) -> None:
+    check(load().pty_batch_apply(C.byref(args), stream_ptr()), "pty_batch_apply")
+
+
+def batch_finalize(err_part, n_visits: int, window: int, err_out) -> None:
+    check(load().pty_batch_finalize(ptr(err_part), n_visits, window, ptr(err_out), stream_ptr()),
+          "pty_batch_finalize")
 
 
 def device_info():

@@ -1,0 +1,7 @@
+// explicit instantiation of the batched extension for float, W = 64
+#include "pty_batched_host.cuh"
+namespace pty {
+template int run_batch_contrib<float, 64>(const PtyBatchArgs*, cudaStream_t);
+template int run_batch_apply<float, 64>(const PtyBatchArgs*, cudaStream_t);
+template int64_t batch_workspace<float, 64>(int, int, int, int, bool);
+}

@@ -14,6 +14,7 @@
 
 #include "pty_register.cuh"
 #include "pty_sweep_host.cuh"
+#include "pty_batched_host.cuh"
 
 namespace pty {
 std::atomic<long long> g_launches{0};
@@ -31,6 +32,42 @@ extern template int run_sweep<double, 64>(const PtySweepArgs*, cudaStream_t);
 extern template int run_sweep<double, 128>(const PtySweepArgs*, cudaStream_t);
 extern template int run_sweep<double, 256>(const PtySweepArgs*, cudaStream_t);
 extern template int run_sweep<double, 512>(const PtySweepArgs*, cudaStream_t);
+extern template int run_batch_contrib<float, 16>(const PtyBatchArgs*, cudaStream_t);
+extern template int run_batch_apply<float, 16>(const PtyBatchArgs*, cudaStream_t);
+extern template int64_t batch_workspace<float, 16>(int, int, int, int, bool);
+extern template int run_batch_contrib<float, 32>(const PtyBatchArgs*, cudaStream_t);
+extern template int run_batch_apply<float, 32>(const PtyBatchArgs*, cudaStream_t);
+extern template int64_t batch_workspace<float, 32>(int, int, int, int, bool);
+extern template int run_batch_contrib<float, 64>(const PtyBatchArgs*, cudaStream_t);
+extern template int run_batch_apply<float, 64>(const PtyBatchArgs*, cudaStream_t);
+extern template int64_t batch_workspace<float, 64>(int, int, int, int, bool);
+extern template int run_batch_contrib<float, 128>(const PtyBatchArgs*, cudaStream_t);
+extern template int run_batch_apply<float, 128>(const PtyBatchArgs*, cudaStream_t);
+extern template int64_t batch_workspace<float, 128>(int, int, int, int, bool);
+extern template int run_batch_contrib<float, 256>(const PtyBatchArgs*, cudaStream_t);
+extern template int run_batch_apply<float, 256>(const PtyBatchArgs*, cudaStream_t);
+extern template int64_t batch_workspace<float, 256>(int, int, int, int, bool);
+extern template int run_batch_contrib<float, 512>(const PtyBatchArgs*, cudaStream_t);
+extern template int run_batch_apply<float, 512>(const PtyBatchArgs*, cudaStream_t);
+extern template int64_t batch_workspace<float, 512>(int, int, int, int, bool);
+extern template int run_batch_contrib<double, 16>(const PtyBatchArgs*, cudaStream_t);
+extern template int run_batch_apply<double, 16>(const PtyBatchArgs*, cudaStream_t);
+extern template int64_t batch_workspace<double, 16>(int, int, int, int, bool);
+extern template int run_batch_contrib<double, 32>(const PtyBatchArgs*, cudaStream_t);
+extern template int run_batch_apply<double, 32>(const PtyBatchArgs*, cudaStream_t);
+extern template int64_t batch_workspace<double, 32>(int, int, int, int, bool);
+extern template int run_batch_contrib<double, 64>(const PtyBatchArgs*, cudaStream_t);
+extern template int run_batch_apply<double, 64>(const PtyBatchArgs*, cudaStream_t);
+extern template int64_t batch_workspace<double, 64>(int, int, int, int, bool);
+extern template int run_batch_contrib<double, 128>(const PtyBatchArgs*, cudaStream_t);
+extern template int run_batch_apply<double, 128>(const PtyBatchArgs*, cudaStream_t);
+extern template int64_t batch_workspace<double, 128>(int, int, int, int, bool);
+extern template int run_batch_contrib<double, 256>(const PtyBatchArgs*, cudaStream_t);
+extern template int run_batch_apply<double, 256>(const PtyBatchArgs*, cudaStream_t);
+extern template int64_t batch_workspace<double, 256>(int, int, int, int, bool);
+extern template int run_batch_contrib<double, 512>(const PtyBatchArgs*, cudaStream_t);
+extern template int run_batch_apply<double, 512>(const PtyBatchArgs*, cudaStream_t);
+extern template int64_t batch_workspace<double, 512>(int, int, int, int, bool);
 }  // namespace pty
 
 using namespace pty;
@@ -288,6 +325,56 @@ int pty_orthogonalize(void* probes, int32_t dtype, int32_t W, int32_t M, void* s
     });
     cudaFreeAsync(work, st);
     return rc;
+}
+
+int64_t pty_batch_workspace_bytes(int32_t dtype, int32_t W, int32_t M, int32_t b, int32_t H, int32_t Wc) {
+    if (!valid_window(W) || M < 1 || M > kMaxBatchModes || b < 1 || H < W || Wc < W) return -1;
+    int64_t out = -1;
+    with_dtype(dtype, [&](auto t) {
+        using T = decltype(t);
+        return with_window(W, [&](auto w) {
+            out = batch_workspace<T, decltype(w)::value>(M, b, H, Wc, true);
+            return PTY_OK;
+        });
+    });
+    return out;
+}
+
+static int batch_check(const PtyBatchArgs* a) {
+    if (!a || !valid_window(a->window) || a->modes < 1 || a->modes > kMaxBatchModes || a->n_batch < 1 ||
+        !a->obj || !a->probes || !a->patterns || !a->positions || !a->batch || !a->obj_acc ||
+        !a->probe_acc || !a->err_part || !a->status || a->H < a->window || a->Wc < a->window ||
+        a->visit0 < 0 || a->visit0 + a->n_batch > a->n_positions)
+        return PTY_ERR_ARGUMENT;
+    if (a->sense != PTY_SENSE_NONE && !a->stage) return PTY_ERR_ARGUMENT;
+    return PTY_OK;
+}
+
+int pty_batch_contrib(const PtyBatchArgs* a, void* stream) {
+    if (int rc = batch_check(a)) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    return with_dtype(a->dtype, [&](auto t) {
+        using T = decltype(t);
+        return with_window(a->window, [&](auto w) { return run_batch_contrib<T, decltype(w)::value>(a, st); });
+    });
+}
+
+int pty_batch_apply(const PtyBatchArgs* a, void* stream) {
+    if (int rc = batch_check(a)) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    return with_dtype(a->dtype, [&](auto t) {
+        using T = decltype(t);
+        return with_window(a->window, [&](auto w) { return run_batch_apply<T, decltype(w)::value>(a, st); });
+    });
+}
+
+int pty_batch_finalize(const double* err_part, int32_t n_visits, int32_t W, double* err_out, void* stream) {
+    if (!err_part || !err_out || n_visits < 1 || !valid_window(W)) return PTY_ERR_ARGUMENT;
+    ErrOut outs{};
+    outs.p[0] = err_out;
+    sweep_finalize_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(err_part, n_visits, W / 4, 1, outs);
+    count();
+    return last_status();
 }
 
 int pty_check_patterns(const void* patterns, int32_t dtype, int64_t count, int32_t* status, void* stream) {

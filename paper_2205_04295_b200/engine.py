@@ -55,6 +55,7 @@ class SolverConfig:
     posref: PosRefConfig | None = None
     track_modulus_error: bool = False
     precision: str = "fp32"           # B200 extension: fp32 (complex64) | fp64 (complex128)
+    batch_size: int = 1               # B200 extension: >1 = batched semi-parallel update
 
     def __post_init__(self) -> None:
         if not (0 <= self.alpha_obj <= 1 and 0 <= self.alpha_probe <= 1):
@@ -69,6 +70,8 @@ class SolverConfig:
             raise ParameterError("mode_count must be <= 8 on the B200 path")
         if self.precision not in ("fp32", "fp64"):
             raise ParameterError(f"precision must be 'fp32' or 'fp64', got {self.precision!r}")
+        if self.batch_size < 1:
+            raise ParameterError("batch_size must be >= 1")
 
 
 class ReconState:
@@ -207,10 +210,120 @@ def _engaged(state: ReconState, config: SolverConfig) -> bool:
     return config.posref is not None and state.iteration >= config.posref.warmup_iterations
 
 
-def sweep(state: ReconState, dataset, config: SolverConfig) -> ReconState:
-    """engine.py:173-243 -- one pass over all positions, mutating ``state``."""
+def sweep(state: ReconState, dataset, config: SolverConfig, group=None) -> ReconState:
+    """engine.py:173-243 -- one pass over all positions, mutating ``state``.
+
+    ``config.batch_size > 1`` selects the batched semi-parallel extension
+    (oracle/batched.py); ``group`` (a torch.distributed process group) then
+    splits every batch across its ranks and all-reduces the update terms."""
+    if config.batch_size > 1:
+        return sweep_batched(state, dataset, config, group)
     sweep_replicas([state], [dataset], config)
     return state
+
+
+def batch_slice(n_batch: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous share [lo, hi) of a batch of n_batch positions for one rank."""
+    base, extra = divmod(n_batch, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def sweep_batched(state: ReconState, dataset, config: SolverConfig, group=None) -> ReconState:
+    """Batched rPIE sweep (extension; b = config.batch_size).  Every batch is a
+    contiguous slice of the visit order; its positions see the batch-start
+    state; numerators/denominators are summed (per rank, then NCCL all-reduce
+    across ``group``) and applied once (pty_batch_contrib / pty_batch_apply)."""
+    t = _native.torch()
+    t0 = time.perf_counter()
+    st, ds = state, dataset
+    w, m = st.window, int(st.probe_stack.shape[0])
+    n = ds.n_positions
+    cdt = st.obj.dtype
+    rdt = t.float32 if cdt == t.complex64 else t.float64
+    dcode = _native.dtype_code(cdt)
+    world, rank = 1, 0
+    if group is not None:
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+    engaged = _engaged(st, config)
+    if engaged and world > 1:
+        raise ParameterError("position refinement with a multi-rank batched sweep is not supported yet")
+    sense = _native.SENSE_NONE
+    if engaged:
+        sense = _native.SENSE_XCORR_A if config.posref.sensor == "XCORR_A" else _native.SENSE_XCORR_B
+    pats = device_patterns(ds, rdt)
+    order = visit_order(n, config, st.iteration)
+    b = min(config.batch_size, n)
+    h, wc = st.obj.shape
+    st.obj = st.obj.contiguous()
+    st.probe_stack = st.probe_stack.contiguous()
+    status = st.buffer("status", (1,), t.int32)
+    status.zero_()
+    err = st.buffer("err", (3,), t.float64)
+    err_part = st.buffer("err_part", (n, w // 4, 3), t.float64)
+    err_part.zero_()
+    obj_acc = st.buffer("obj_acc", (3, h, wc), rdt)
+    probe_acc = st.buffer("probe_acc", (2 * m + 1, w, w), rdt)
+    stage = st.buffer("stage", (n, 2, w, w), cdt) if engaged else None
+    order_h = st.buffer("order", (n,), t.int32, pinned=True)
+    order_h.numpy()[:] = order
+    order_d = st.buffer("order", (n,), t.int32)
+    order_d.copy_(order_h, non_blocking=True)
+    ws = _native.workspace(_native.batch_workspace_bytes(dcode, w, m, b, h, wc), "batch")
+    upd_probe = int(bool(config.update_probe_modes) and config.alpha_probe > 0)
+    for s in range(0, n, b):
+        nb = min(b, n - s)
+        lo, hi = batch_slice(nb, rank, world)
+        if hi > lo:
+            args = _native.PtyBatchArgs(
+                dcode, w, m, n, _native.ptr(st.obj), h, wc, st.canvas_origin[0], st.canvas_origin[1],
+                _native.ptr(st.probe_stack), _native.ptr(pats), _native.ptr(st.positions),
+                _native.ptr(order_d) + 4 * (s + lo), hi - lo, s + lo,
+                float(config.alpha_obj), float(config.alpha_probe), float(config.beta),
+                float(config.gamma), float(config.epsilon_rel), upd_probe,
+                int(bool(config.track_modulus_error)), sense, _native.ptr(stage),
+                _native.ptr(obj_acc), _native.ptr(probe_acc), _native.ptr(err_part),
+                _native.ptr(status), _native.ptr(ws), ws.numel())
+            _native.batch_contrib(args)
+        else:
+            obj_acc.zero_()
+            probe_acc.zero_()
+        if world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(obj_acc, group=group)
+            dist.all_reduce(probe_acc, group=group)
+        args = _native.PtyBatchArgs(
+            dcode, w, m, n, _native.ptr(st.obj), h, wc, st.canvas_origin[0], st.canvas_origin[1],
+            _native.ptr(st.probe_stack), _native.ptr(pats), _native.ptr(st.positions),
+            _native.ptr(order_d) + 4 * (s + lo), max(hi - lo, 1), s + min(lo, nb - 1),
+            float(config.alpha_obj), float(config.alpha_probe), float(config.beta),
+            float(config.gamma), float(config.epsilon_rel), upd_probe,
+            int(bool(config.track_modulus_error)), sense, _native.ptr(stage),
+            _native.ptr(obj_acc), _native.ptr(probe_acc), _native.ptr(err_part),
+            _native.ptr(status), _native.ptr(ws), ws.numel())
+        _native.batch_apply(args)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(err_part, group=group)
+        dist.all_reduce(status, op=dist.ReduceOp.MAX, group=group)
+    _native.batch_finalize(err_part, n, w, err)
+    if engaged:
+        _refine_positions(st, config.posref, n, w)
+    if (config.ortho_interval > 0 and m > 1 and (st.iteration + 1) % config.ortho_interval == 0):
+        _native.orthogonalize(st.probe_stack)
+    he = st.buffer("err", (3,), t.float64, pinned=True)
+    hs = st.buffer("status", (1,), t.int32, pinned=True)
+    he.copy_(err, non_blocking=True)
+    hs.copy_(status, non_blocking=True)
+    t.cuda.current_stream().synchronize()
+    raise_for_status(int(hs.numpy()[0]), "batched sweep")
+    num, den, worst = he.numpy()
+    st.error_trace.append(float(num) / max(float(den), TINY))
+    if config.track_modulus_error:
+        st.modulus_error_trace.append(float(worst))
+    st.seconds_per_iteration.append(time.perf_counter() - t0)
+    return st
 
 
 def sweep_replicas(states, datasets, config: SolverConfig, orders=None, kernel_events=None):
