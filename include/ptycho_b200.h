@@ -68,6 +68,7 @@ typedef struct PtySlot {
     int32_t        r0, c0;       /* canvas origin (engine.py:77-81)                 */
     void*          probes;       /* [M][W][W] complex, updated in place             */
     const void*    patterns;     /* [N][W][W] real (measured intensity I)           */
+    const void*    patterns_t;   /* [N][W][W] real, each pattern transposed         */
     const double*  positions;    /* [N][2] (x, y) float64                           */
     const int32_t* order;        /* [N] visit order of this sweep (engine.py:177-181) */
     void*          stage;        /* posref staging [N][2][W][W] complex or NULL     */
@@ -166,7 +167,9 @@ PTY_API int pty_check_patterns(const void* patterns, int32_t dtype, int64_t coun
  *   probe_acc [2M+1][W][W] real: probe numerator (re, im) per mode, denominator
  * (real = float for PTY_DTYPE_C64, double for C128).  Ranks that split a batch
  * all-reduce (sum) both accumulators, then every rank calls pty_batch_apply.
- * err_part [n_positions][W/4][3] is indexed by visit rank (visit0 + k) and
+ * patterns_t is the diffraction stack transposed per pattern (I^T[j][kc][u]),
+ * the layout the column passes stream.
+ * err_part [n_positions][W][3] is indexed by visit rank (visit0 + k) and
  * reduced once per sweep by pty_batch_finalize (deterministic order).
  */
 typedef struct PtyBatchArgs {
@@ -175,6 +178,7 @@ typedef struct PtyBatchArgs {
     int32_t H, Wc, r0, c0;
     void*   probes;
     const void*    patterns;     /* [N][W][W] real                              */
+    const void*    patterns_t;   /* [N][W][W] real, each pattern transposed     */
     const double*  positions;    /* [N][2] (x, y) float64                       */
     const int32_t* batch;        /* [n_batch] position ids (this rank's slice)  */
     int32_t n_batch, visit0;

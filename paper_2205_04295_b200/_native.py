@@ -45,8 +45,9 @@ def stream_ptr() -> int:
 class PtySlot(C.Structure):
     _fields_ = [("obj", C.c_void_p), ("H", C.c_int32), ("Wc", C.c_int32),
                 ("r0", C.c_int32), ("c0", C.c_int32), ("probes", C.c_void_p),
-                ("patterns", C.c_void_p), ("positions", C.c_void_p), ("order", C.c_void_p),
-                ("stage", C.c_void_p), ("err_out", C.c_void_p), ("status", C.c_void_p)]
+                ("patterns", C.c_void_p), ("patterns_t", C.c_void_p), ("positions", C.c_void_p),
+                ("order", C.c_void_p), ("stage", C.c_void_p), ("err_out", C.c_void_p),
+                ("status", C.c_void_p)]
 
 
 class PtySweepArgs(C.Structure):
@@ -63,8 +64,8 @@ class PtyBatchArgs(C.Structure):
     _fields_ = [("dtype", C.c_int32), ("window", C.c_int32), ("modes", C.c_int32),
                 ("n_positions", C.c_int32), ("obj", C.c_void_p), ("H", C.c_int32), ("Wc", C.c_int32),
                 ("r0", C.c_int32), ("c0", C.c_int32), ("probes", C.c_void_p),
-                ("patterns", C.c_void_p), ("positions", C.c_void_p), ("batch", C.c_void_p),
-                ("n_batch", C.c_int32), ("visit0", C.c_int32),
+                ("patterns", C.c_void_p), ("patterns_t", C.c_void_p), ("positions", C.c_void_p),
+                ("batch", C.c_void_p), ("n_batch", C.c_int32), ("visit0", C.c_int32),
                 ("alpha_obj", C.c_double), ("alpha_probe", C.c_double), ("beta", C.c_double),
                 ("gamma", C.c_double), ("epsilon_rel", C.c_double),
                 ("update_probe", C.c_int32), ("track_modulus", C.c_int32), ("sense", C.c_int32),

@@ -19,7 +19,7 @@
 //   -- accumulators may be all-reduced across ranks here (NCCL) --
 //   bk_obj_tile_max, bk_obj_apply, bk_probe_apply, bk_stage_after
 #pragma once
-#include "pty_fft.cuh"
+#include "pty_tasks.cuh"
 
 namespace pty {
 
@@ -30,10 +30,12 @@ constexpr int kMaxBatchModes = 8;
 struct BatchDev {
     int W, M, N, b;                    // window, modes, positions in dataset, positions in batch
     int TR, TC, lgTR, lgTC, nRT, nCT, G;
+    int accumulate;                    // chunks after the first add into pgroup
     void* obj;
     int H, Wc, r0, c0;
     void* probes;
     const void* patterns;
+    const void* patternsT;             // [N][W][W] real, transposed (I^T[j][kc][u])
     const double* positions;
     const int* batch;                  // [b] position ids
     int visit0;                        // index of batch[0] in the sweep's visit order
@@ -42,16 +44,17 @@ struct BatchDev {
     void* stage;                       // [N][2][W][W] complex or null
     void* obj_acc;                     // [3][H][Wc] real: num.re, num.im, den
     void* probe_acc;                   // [2M+1][W][W] real: pnum (re, im) per mode, pden
-    double* err_part;                  // [N][nCT][3] by visit rank (visit0 + k)
+    double* err_part;                  // [N][W][3] by visit rank (visit0 + k)
     int* status;
     // workspace
     int* anchors;                      // [b][2]
     void* scratch;                     // [b][M][W][W] complex
-    void* onum;                        // [b][W][W] complex
+    void* onum;                        // [b][M][W][W] complex: per-mode object numerators
     void* pp;                          // [W][W] real (probe power)
     void* pp_part;                     // [nRT] real
-    void* omax_part;                   // [b][nRT] real
-    void* tmax_part;                   // [b][nCT] real
+    void* omax_part;                   // [b][W/4] real (per row quad)
+    void* tmax_part;                   // [b][W] real (per column)
+    void* totT;                        // [b][W][W] real: total^T
     void* pgroup;                      // [G][2M+1][W][W] real
     void* tile_max;                    // [ntiles] real
     void* upd;                         // [H][Wc] complex (posref staging only) or null
@@ -96,276 +99,184 @@ __global__ void __launch_bounds__(kBatThreads) bk_probe_power(const __grid_const
     }
 }
 
-// K1: gather + exit waves + row DFTs.  CTA = (position k, row tile).
+// ---------------------------------------------------------------------------
+// Line-task kernels.  A "group" is B threads transforming one line with the
+// fused-I/O group_fft; a "team" is 4 groups that own 4 consecutive rows, so a
+// transposed scratch access moves 4 consecutive complex values (one 32-byte
+// sector) per column.  Scratch layout after the row pass: [k][m][kc][r]
+// (row-DFT output transposed), so column passes read contiguous lines.
+// CTAs are persistent over tasks; no CTA-wide barrier inside a task.
+
+constexpr int kLineThreads = 128;
+
+// K1: exit waves C * P_m * o_j and row DFTs (engine.py:113, fields.py:81).
+// Team task (k, m, row quad); output transposed into scratch.
 template <typename T, int W>
-__global__ void __launch_bounds__(kBatThreads) bk_rows_fwd(const __grid_constant__ BatchDev P) {
+__global__ void __launch_bounds__(kLineThreads) bk_rows_fwd(const __grid_constant__ BatchDev P) {
     using C = cplx<T>;
-    constexpr int LS = line_stride<W>();
+    constexpr int B = Shape<W>::B, TEAM = 4 * B, NTEAM = kLineThreads / TEAM, XS = xch_size<W>();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* tw = reinterpret_cast<C*>(smem_raw);
-    T* red = reinterpret_cast<T*>(tw + W);
-    C* tile = reinterpret_cast<C*>(red + 64);
+    C* xch_all = tw + W;
+    C* tt_all = xch_all + (kLineThreads / B) * XS;
+    T* red = reinterpret_cast<T*>(tt_all + NTEAM * W * 5);
     load_twiddles<T, W>(tw, reinterpret_cast<const C*>(P.twiddles));
-    const int k = blockIdx.x / P.nRT, rt = blockIdx.x % P.nRT;
+    __syncthreads();
     if (*(volatile const int*)P.status) return;
-    const int M = P.M, NT = blockDim.x;
+    const int team = threadIdx.x / TEAM, tl = threadIdx.x % TEAM, gi = tl / B, b = tl % B;
+    const unsigned gmask = group_mask<W>();
+    C* xch = xch_all + (threadIdx.x / B) * XS;
+    C* tt = tt_all + team * W * 5;
+    const int M = P.M, nq = W / 4, ntasks = P.b * M * nq;
     const size_t WW = (size_t)W * W;
-    const int j = P.batch[k], ar = P.anchors[2 * k], ac = P.anchors[2 * k + 1];
     const C* obj = reinterpret_cast<const C*>(P.obj);
     const C* probes = reinterpret_cast<const C*>(P.probes);
-    const T* I = reinterpret_cast<const T*>(P.patterns) + (size_t)j * WW;
-    for (size_t q = threadIdx.x; q < (size_t)P.TR * W * sizeof(T) / 128; q += NT)   // pattern rows -> L2
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(I + (size_t)rt * P.TR * W) + q * 128));
-    C* stg = P.sense == PTY_SENSE_XCORR_A ? reinterpret_cast<C*>(P.stage) + (size_t)j * 2 * WW : nullptr;
-    T om = T(0);
-    constexpr int U = 4;
-    const int nel = P.TR * M * W;
-    for (int i0 = threadIdx.x; i0 < nel; i0 += NT * U) {
-        C o[U], p[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int i = i0 + u * NT;
-            if (i < nel) {
-                const int l = i / W, c = i % W, m = l >> P.lgTR, rr = rt * P.TR + (l & (P.TR - 1));
-                o[u] = obj[(size_t)(ar + rr) * P.Wc + ac + c];
-                p[u] = probes[m * WW + (size_t)rr * W + c];
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int i = i0 + u * NT;
-            if (i < nel) {
-                const int l = i / W, c = i % W, m = l >> P.lgTR, rr = rt * P.TR + (l & (P.TR - 1));
-                if (m == 0) {
-                    om = fmax(om, norm2(o[u]));
-                    if (stg) stg[(size_t)rr * W + c] = o[u];          // sensor input o_j (posref.py:66)
-                }
-                tile[(size_t)l * LS + pad<W>(c)] = scale(p[u] * o[u], checker<T>(rr, c));
-            }
-        }
-    }
-    om = block_max(om, red);
-    if (threadIdx.x == 0) reinterpret_cast<T*>(P.omax_part)[(size_t)k * P.nRT + rt] = om;
-    __syncthreads();
-    lines_fft<T, W, false>(tile, P.TR * M, LS, tw);
-    __syncthreads();
-    C* scr = reinterpret_cast<C*>(P.scratch) + (size_t)k * M * WW;
-    for (int i = threadIdx.x; i < P.TR * M * W; i += NT) {
-        const int l = i / W, c = i % W;
-        scr[(l >> P.lgTR) * WW + (size_t)(rt * P.TR + (l & (P.TR - 1))) * W + c] = tile[(size_t)l * LS + pad<W>(c)];
+    C* scratch = reinterpret_cast<C*>(P.scratch);
+    for (int task = blockIdx.x * NTEAM + team; task < ntasks; task += gridDim.x * NTEAM) {
+        const int k = task / (M * nq), rem = task % (M * nq), m = rem / nq, rq = rem % nq;
+        const int j = P.batch[k];
+        C* stg = (P.sense == PTY_SENSE_XCORR_A && m == 0) ? reinterpret_cast<C*>(P.stage) + (size_t)j * 2 * WW : nullptr;
+        const T om = task_row_fwd<T, W>(tw, xch, tt, red + team * 4, team, tl, gi, b, gmask, obj, P.Wc,
+                                        P.anchors[2 * k], P.anchors[2 * k + 1], probes, m, rq,
+                                        scratch + (size_t)k * M * WW, stg);
+        if (m == 0 && tl == 0) reinterpret_cast<T*>(P.omax_part)[(size_t)k * nq + rq] = om;
     }
 }
 
-// column tile <-> padded lines (mode-major lines m*TC + cc)
+// K2: column DFTs of every mode, Psi written back in place, total^T and
+// max(total) partial per column (engine.py:114-117).  Group task (k, kc).
 template <typename T, int W>
-__device__ __forceinline__ void bk_load_cols(cplx<T>* tile, const cplx<T>* scr, int M, int TC, int lgTC, int ct) {
-    constexpr int LS = line_stride<W>(), U = 8;
-    const size_t WW = (size_t)W * W;
-    const int nel = M * W * TC;
-    for (int i0 = threadIdx.x; i0 < nel; i0 += blockDim.x * U) {
-        cplx<T> v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int i = i0 + u * blockDim.x;
-            if (i < nel) {
-                const int rem = i & ((W << lgTC) - 1), m = i >> (lgTC + Log2<W>::value);
-                v[u] = scr[m * WW + (size_t)(rem >> lgTC) * W + ct * TC + (rem & (TC - 1))];
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int i = i0 + u * blockDim.x;
-            if (i < nel) {
-                const int rem = i & ((W << lgTC) - 1), m = i >> (lgTC + Log2<W>::value);
-                tile[(size_t)((m << lgTC) + (rem & (TC - 1))) * LS + pad<W>(rem >> lgTC)] = v[u];
-            }
-        }
-    }
-}
-template <typename T, int W>
-__device__ __forceinline__ void bk_store_cols(const cplx<T>* tile, cplx<T>* scr, int M, int TC, int lgTC, int ct) {
-    constexpr int LS = line_stride<W>();
-    const size_t WW = (size_t)W * W;
-    for (int i = threadIdx.x; i < M * W * TC; i += blockDim.x) {
-        const int rem = i & ((W << lgTC) - 1), m = i >> (lgTC + Log2<W>::value);
-        const int r = rem >> lgTC, cc = rem & (TC - 1);
-        scr[m * WW + (size_t)r * W + ct * TC + cc] = tile[(size_t)((m << lgTC) + cc) * LS + pad<W>(r)];
-    }
-}
-
-// K2: column DFTs; Psi stored back; max(total) partials (engine.py:114-117)
-template <typename T, int W>
-__global__ void __launch_bounds__(kBatThreads) bk_cols_fwd(const __grid_constant__ BatchDev P) {
+__global__ void __launch_bounds__(kLineThreads) bk_cols_fwd(const __grid_constant__ BatchDev P) {
     using C = cplx<T>;
-    constexpr int LS = line_stride<W>();
+    constexpr int A = Shape<W>::A, B = Shape<W>::B, NG = kLineThreads / B, XS = xch_size<W>();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* tw = reinterpret_cast<C*>(smem_raw);
-    T* red = reinterpret_cast<T*>(tw + W);
-    C* tile = reinterpret_cast<C*>(red + 64);
+    C* xch = tw + W + (threadIdx.x / B) * XS;
     load_twiddles<T, W>(tw, reinterpret_cast<const C*>(P.twiddles));
+    __syncthreads();
     if (*(volatile const int*)P.status) return;
-    const int k = blockIdx.x / P.nCT, ct = blockIdx.x % P.nCT, M = P.M;
-    C* scr = reinterpret_cast<C*>(P.scratch) + (size_t)k * M * W * W;
-    bk_load_cols<T, W>(tile, scr, M, P.TC, P.lgTC, ct);
-    __syncthreads();
-    lines_fft<T, W, false>(tile, M * P.TC, LS, tw);
-    __syncthreads();
+    const int grp = threadIdx.x / B, b = threadIdx.x % B;
+    const unsigned gmask = group_mask<W>();
+    const int M = P.M;
+    const size_t WW = (size_t)W * W;
     const T invW2 = T(1) / (T(W) * T(W));
-    T tm = T(0);
-    for (int i = threadIdx.x; i < W * P.TC; i += blockDim.x) {
-        const int cc = i / W, r = i % W;
-        T tot = T(0);
-        for (int m = 0; m < M; ++m) tot += norm2(tile[(size_t)(m * P.TC + cc) * LS + pad<W>(r)]) * invW2;
-        tm = fmax(tm, tot);
+    C* scratch = reinterpret_cast<C*>(P.scratch);
+    T* totT = reinterpret_cast<T*>(P.totT);
+    for (int task = blockIdx.x * NG + grp; task < P.b * W; task += gridDim.x * NG) {
+        const int k = task / W, kc = task % W;
+        const T tm = task_col_fwd<T, W>(tw, xch, b, gmask, scratch + (size_t)k * M * WW, M, kc, totT + (size_t)k * WW);
+        if (b == 0) reinterpret_cast<T*>(P.tmax_part)[(size_t)k * W + kc] = tm;
     }
-    tm = block_max(tm, red);
-    if (threadIdx.x == 0) reinterpret_cast<T*>(P.tmax_part)[(size_t)k * P.nCT + ct] = tm;
-    bk_store_cols<T, W>(tile, scr, M, P.TC, P.lgTC, ct);
 }
 
-// K3: modulus constraint (engine.py:117-119), error terms (engine.py:198-202),
-// inverse column DFTs
+// K3: modulus constraint scale = sqrt(I)/sqrt(total + eps) (engine.py:117-118),
+// error terms (engine.py:198-214), inverse column DFTs.  Group task (k, kc).
 template <typename T, int W>
-__global__ void __launch_bounds__(kBatThreads) bk_cols_mod(const __grid_constant__ BatchDev P) {
+__global__ void __launch_bounds__(kLineThreads) bk_cols_mod(const __grid_constant__ BatchDev P) {
     using C = cplx<T>;
-    constexpr int LS = line_stride<W>();
+    constexpr int A = Shape<W>::A, B = Shape<W>::B, NG = kLineThreads / B, XS = xch_size<W>();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* tw = reinterpret_cast<C*>(smem_raw);
-    T* red = reinterpret_cast<T*>(tw + W);
-    C* tile = reinterpret_cast<C*>(red + 64);
+    C* xch = tw + W + (threadIdx.x / B) * XS;
     load_twiddles<T, W>(tw, reinterpret_cast<const C*>(P.twiddles));
+    __syncthreads();
     if (*(volatile const int*)P.status) return;
-    const int k = blockIdx.x / P.nCT, ct = blockIdx.x % P.nCT, M = P.M;
+    const int grp = threadIdx.x / B, b = threadIdx.x % B;
+    const unsigned gmask = group_mask<W>();
+    const int M = P.M;
     const size_t WW = (size_t)W * W;
-    const int j = P.batch[k];
-    C* scr = reinterpret_cast<C*>(P.scratch) + (size_t)k * M * WW;
-    bk_load_cols<T, W>(tile, scr, M, P.TC, P.lgTC, ct);
-    const T tmax = bk_max_of(reinterpret_cast<const T*>(P.tmax_part) + (size_t)k * P.nCT, P.nCT);
-    const T eps = T(P.eps_rel) * fmax(tmax, real_limits<T>::tiny());
-    const T* I = reinterpret_cast<const T*>(P.patterns) + (size_t)j * WW;
-    C* stg = P.sense == PTY_SENSE_XCORR_B ? reinterpret_cast<C*>(P.stage) + (size_t)j * 2 * WW : nullptr;
     const T invW2 = T(1) / (T(W) * T(W));
-    __syncthreads();
-    double en = 0.0, ed = 0.0;
-    T worst = T(0);
-    for (int i = threadIdx.x; i < W * P.TC; i += blockDim.x) {
-        const int r = i >> P.lgTC, cc = i & (P.TC - 1), c = ct * P.TC + cc;
-        T tot = T(0);
-        for (int m = 0; m < M; ++m) tot += norm2(tile[(size_t)(m * P.TC + cc) * LS + pad<W>(r)]) * invW2;
-        const T Iv = I[(size_t)r * W + c];
-        const T sI = sqrt_rn(Iv);
-        const T sc = sI / sqrt_rn(tot + eps);
-        const T d = sqrt_rn(tot) - sI;
-        en += (double)(d * d);
-        ed += (double)Iv;
-        T after = T(0);
-        for (int m = 0; m < M; ++m) {
-            C& a = tile[(size_t)(m * P.TC + cc) * LS + pad<W>(r)];
-            a = scale(a, sc);
-            after += norm2(a) * invW2;
-        }
-        if (P.track_mod && tot > T(1e-3) * tmax) worst = fmax(worst, fabs(after - Iv) / fmax(Iv, real_limits<T>::tiny()));
-        if (stg) {
-            stg[(size_t)r * W + c] = C{tot, T(0)};
-            stg[WW + (size_t)r * W + c] = C{Iv, T(0)};
-        }
+    C* scratch = reinterpret_cast<C*>(P.scratch);
+    const T* totT = reinterpret_cast<const T*>(P.totT);
+    for (int task = blockIdx.x * NG + grp; task < P.b * W; task += gridDim.x * NG) {
+        const int k = task / W, kc = task % W, j = P.batch[k];
+        C* stg = P.sense == PTY_SENSE_XCORR_B ? reinterpret_cast<C*>(P.stage) + (size_t)j * 2 * WW : nullptr;
+        task_col_mod<T, W>(tw, xch, b, gmask, scratch + (size_t)k * M * WW, M, kc, totT + (size_t)k * WW,
+                           reinterpret_cast<const T*>(P.tmax_part) + (size_t)k * W,
+                           reinterpret_cast<const T*>(P.patternsT) + (size_t)j * WW, T(P.eps_rel), P.track_mod, stg,
+                           P.err_part + ((size_t)(P.visit0 + k) * W + kc) * 3);
     }
-    __syncthreads();
-    lines_fft<T, W, true>(tile, M * P.TC, LS, tw);
-    __syncthreads();
-    double* dred = reinterpret_cast<double*>(red);
-    en = block_sum(en, dred);
-    ed = block_sum(ed, dred);
-    worst = block_max(worst, red);
-    if (threadIdx.x == 0) {
-        double* e = P.err_part + ((size_t)(P.visit0 + k) * P.nCT + ct) * 3;
-        e[0] = en;
-        e[1] = ed;
-        e[2] = (double)worst;
-    }
-    bk_store_cols<T, W>(tile, scr, M, P.TC, P.lgTC, ct);
 }
 
-// K4: inverse row DFTs and the update contributions.  CTA = (row tile, group g);
-// it walks the positions k = g, g + G, ... in order, so its probe partial is a
-// fixed-order sum.  Probe accumulators for the tile rows live in shared memory.
+// K4: inverse row DFTs and the update terms.  Team task (row quad, mode m,
+// position group g): the team walks positions k = g, g+G, ... of the chunk in
+// order, writes the per-mode object numerator onum[k][m] and keeps mode m's
+// probe numerator (and, for m = 0, the probe denominator) in shared memory --
+// a fixed-order, atomic-free reduction.
 template <typename T, int W>
-__global__ void __launch_bounds__(kBatThreads) bk_rows_inv(const __grid_constant__ BatchDev P) {
+__global__ void bk_rows_inv(const __grid_constant__ BatchDev P) {
     using C = cplx<T>;
-    constexpr int LS = line_stride<W>();
+    constexpr int A = Shape<W>::A, B = Shape<W>::B, TEAM = 4 * B, LS4 = team_line_stride<W>();
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int M = P.M;
     C* tw = reinterpret_cast<C*>(smem_raw);
-    T* red = reinterpret_cast<T*>(tw + W);
-    C* tile = reinterpret_cast<C*>(red + 64);
-    const int M = P.M, NT = blockDim.x;
-    C* pnum = tile + (size_t)P.TR * M * LS;                  // [M][TR*W]
-    T* pden = reinterpret_cast<T*>(pnum + (size_t)M * P.TR * W);   // [TR*W]
+    C* lines = tw + W;                                         // [4][LS4]
+    C* pnum = lines + 4 * LS4;                                 // [4][W] (mode m)
+    T* pden = reinterpret_cast<T*>(pnum + 4 * W);             // [4][W]
     load_twiddles<T, W>(tw, reinterpret_cast<const C*>(P.twiddles));
+    __syncthreads();
     if (*(volatile const int*)P.status) return;
-    const int rt = blockIdx.x % P.nRT, g = blockIdx.x / P.nRT;
+    const int tl = threadIdx.x, gi = tl / B, b = tl % B;
+    const unsigned gmask = group_mask<W>();
+    const int nq = W / 4;
     const size_t WW = (size_t)W * W;
-    const int npx = P.TR * W;
-    for (int i = threadIdx.x; i < M * npx; i += NT) pnum[i] = C{T(0), T(0)};
-    for (int i = threadIdx.x; i < npx; i += NT) pden[i] = T(0);
-    const C* obj = reinterpret_cast<const C*>(P.obj);
-    const C* probes = reinterpret_cast<const C*>(P.probes);
     const T invW2 = T(1) / (T(W) * T(W));
     const T alpha_p = T(P.alpha_p), beta = T(P.beta);
-    for (int k = g; k < P.b; k += P.G) {
-        const C* scr = reinterpret_cast<const C*>(P.scratch) + (size_t)k * M * WW;
-        __syncthreads();
-        constexpr int U = 8;
-        const int nel = P.TR * M * W;
-        for (int i0 = threadIdx.x; i0 < nel; i0 += NT * U) {
-            C v[U];
+    const C* obj = reinterpret_cast<const C*>(P.obj);
+    const C* probes = reinterpret_cast<const C*>(P.probes);
+    const C* scratch = reinterpret_cast<const C*>(P.scratch);
+    C* myline = lines + gi * LS4;
+    for (int task = blockIdx.x; task < nq * M * P.G; task += gridDim.x) {
+        const int rq = task % nq, m = (task / nq) % M, g = task / (nq * M), r = 4 * rq + gi;
+        T* pg = reinterpret_cast<T*>(P.pgroup) + (size_t)g * (2 * M + 1) * WW + (size_t)4 * rq * W;
+        const bool den_owner = P.update_probe && m == 0;
+        for (int i = tl; i < 4 * W; i += TEAM) {
+            pnum[i] = P.accumulate ? C{pg[(size_t)(2 * m) * WW + i], pg[(size_t)(2 * m + 1) * WW + i]} : C{T(0), T(0)};
+            if (den_owner) pden[i] = P.accumulate ? pg[(size_t)(2 * M) * WW + i] : T(0);
+        }
+        C pv[A];                                               // P_m(r, c) for my output columns
+        const C* prow = probes + m * WW + (size_t)r * W;
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int i = i0 + u * NT;
-                if (i < nel) {
-                    const int l = i / W, c = i % W;
-                    v[u] = scr[(l >> P.lgTR) * WW + (size_t)(rt * P.TR + (l & (P.TR - 1))) * W + c];
-                }
+        for (int q = 0; q < A; ++q) pv[q] = prow[b + B * (q / B) + A * (q % B)];
+        for (int k = g; k < P.b; k += P.G) {
+            const int ar = P.anchors[2 * k], ac = P.anchors[2 * k + 1];
+            const T* op = reinterpret_cast<const T*>(P.omax_part) + (size_t)k * nq;
+            T omax = T(0);
+            for (int q = b; q < nq; q += B) omax = fmax(omax, op[q]);
+            omax = group_max<B>(omax);
+            if (P.update_probe && omax == T(0)) {              // engine.py:145-147
+                if (tl == 0) atomicOr(P.status, PTY_ERR_OBJECT_ZERO);
+                continue;
             }
+            const C* src = scratch + ((size_t)k * M + m) * WW + 4 * rq;
+            const C* orow = obj + (size_t)(ar + r) * P.Wc + ac;
+            team_sync<TEAM>(0);                                // previous FFT done with `lines`
+            for (int e = tl; e < 4 * W; e += TEAM) lines[(e & 3) * LS4 + pad<W>(e >> 2)] = src[(size_t)(e >> 2) * W + (e & 3)];
+            C ov[A];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int i = i0 + u * NT;
-                if (i < nel) tile[(size_t)(i / W) * LS + pad<W>(i % W)] = v[u];
-            }
+            for (int q = 0; q < A; ++q) ov[q] = orow[b + B * (q / B) + A * (q % B)];
+            team_sync<TEAM>(0);
+            C* on = reinterpret_cast<C*>(P.onum) + ((size_t)k * M + m) * WW + (size_t)r * W;
+            group_fft<T, W, true>(
+                myline, tw, b, gmask, [&](int n, int) { return myline[pad<W>(n)]; },
+                [&](int c, int slot, C X) {
+                    const C o = ov[slot];
+                    const C d = scale(X, checker<T>(r, c) * invW2) - pv[slot] * o;
+                    on[c] = mulc(d, pv[slot]);                             // engine.py:130-131
+                    if (P.update_probe) {
+                        C& acc = pnum[gi * W + c];
+                        acc = acc + mulc(scale(d, alpha_p), o);            // engine.py:150
+                        if (m == 0) pden[gi * W + c] += beta * omax + (T(1) - beta) * norm2(o);   // engine.py:148
+                    }
+                });
         }
-        __syncthreads();
-        lines_fft<T, W, true>(tile, P.TR * M, LS, tw);
-        __syncthreads();
-        const int ar = P.anchors[2 * k], ac = P.anchors[2 * k + 1];
-        const T omax = bk_max_of(reinterpret_cast<const T*>(P.omax_part) + (size_t)k * P.nRT, P.nRT);
-        if (P.update_probe && omax == T(0)) {            // engine.py:145-147
-            if (threadIdx.x == 0) atomicOr(P.status, PTY_ERR_OBJECT_ZERO);
-            continue;
+        team_sync<TEAM>(0);
+        for (int i = tl; i < 4 * W; i += TEAM) {
+            pg[(size_t)(2 * m) * WW + i] = pnum[i].re;
+            pg[(size_t)(2 * m + 1) * WW + i] = pnum[i].im;
+            if (den_owner) pg[(size_t)(2 * M) * WW + i] = pden[i];
         }
-        C* onum = reinterpret_cast<C*>(P.onum) + (size_t)k * WW;
-        for (int i = threadIdx.x; i < npx; i += NT) {
-            const int r = i / W, c = i % W, rr = rt * P.TR + r;
-            const C o = obj[(size_t)(ar + rr) * P.Wc + ac + c];
-            const T sg = checker<T>(rr, c) * invW2;
-            C numer{T(0), T(0)};
-            for (int m = 0; m < M; ++m) {
-                const C pv = probes[m * WW + (size_t)rr * W + c];
-                const C d = scale(tile[(size_t)((m << P.lgTR) + r) * LS + pad<W>(c)], sg) - pv * o;
-                numer = numer + mulc(d, pv);                                   // engine.py:130-131
-                if (P.update_probe) pnum[(size_t)m * npx + i] = pnum[(size_t)m * npx + i] + mulc(scale(d, alpha_p), o);
-            }
-            onum[(size_t)rr * W + c] = numer;
-            if (P.update_probe) pden[i] += beta * omax + (T(1) - beta) * norm2(o);   // engine.py:148
-        }
-    }
-    __syncthreads();
-    T* pg = reinterpret_cast<T*>(P.pgroup) + (size_t)g * (2 * M + 1) * WW;
-    for (int i = threadIdx.x; i < npx; i += NT) {
-        const size_t off = (size_t)rt * npx + i;
-        for (int m = 0; m < M; ++m) {
-            pg[(size_t)(2 * m) * WW + off] = pnum[(size_t)m * npx + i].re;
-            pg[(size_t)(2 * m + 1) * WW + off] = pnum[(size_t)m * npx + i].im;
-        }
-        pg[(size_t)(2 * M) * WW + off] = pden[i];
+        team_sync<TEAM>(0);
     }
 }
 
@@ -414,6 +325,7 @@ __global__ void __launch_bounds__(256) bk_obj_gather(const __grid_constant__ Bat
         if (threadIdx.x == 0) for (int w = 0; w < (int)(blockDim.x >> 5); ++w) total += wcount[w];
         __syncthreads();
     }
+    if (total == 0) return;
     const T* pp = reinterpret_cast<const T*>(P.pp);
     const T peak = bk_max_of(reinterpret_cast<const T*>(P.pp_part), P.nRT);
     if (peak == T(0)) {                                       // engine.py:132-134
@@ -421,7 +333,7 @@ __global__ void __launch_bounds__(256) bk_obj_gather(const __grid_constant__ Bat
         return;
     }
     const T gamma = T(P.gamma);
-    const C* onum = reinterpret_cast<const C*>(P.onum);
+    const C* onum = reinterpret_cast<const C*>(P.onum);      // [k][m][W][W]
     T* acc = reinterpret_cast<T*>(P.obj_acc);
     const size_t HW = (size_t)P.H * P.Wc;
     const size_t WW = (size_t)W * W;
@@ -438,7 +350,9 @@ __global__ void __launch_bounds__(256) bk_obj_gather(const __grid_constant__ Bat
             const int p = threadIdx.x + q * 256, R = R0 + p / kObjTile, Cc = C0 + p % kObjTile;
             const int r = R - ar, c = Cc - ac;
             if (R < P.H && Cc < P.Wc && r >= 0 && r < W && c >= 0 && c < W) {
-                num[q] = num[q] + onum[(size_t)k * WW + (size_t)r * W + c];
+                C s = onum[(size_t)k * P.M * WW + (size_t)r * W + c];
+                for (int m = 1; m < P.M; ++m) s = s + onum[((size_t)k * P.M + m) * WW + (size_t)r * W + c];
+                num[q] = num[q] + s;
                 den[q] += gamma * peak + (T(1) - gamma) * pp[(size_t)r * W + c];
             }
         }
@@ -448,9 +362,9 @@ __global__ void __launch_bounds__(256) bk_obj_gather(const __grid_constant__ Bat
         const int p = threadIdx.x + q * 256, R = R0 + p / kObjTile, Cc = C0 + p % kObjTile;
         if (R < P.H && Cc < P.Wc) {
             const size_t o = (size_t)R * P.Wc + Cc;
-            acc[o] = num[q].re;
-            acc[HW + o] = num[q].im;
-            acc[2 * HW + o] = den[q];
+            acc[o] += num[q].re;                      // chunks add in a fixed order
+            acc[HW + o] += num[q].im;
+            acc[2 * HW + o] += den[q];
         }
     }
 }

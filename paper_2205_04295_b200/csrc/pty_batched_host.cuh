@@ -9,39 +9,49 @@ namespace pty {
 
 struct BatchLayout {
     int* anchors;
-    void *scratch, *onum, *pp, *pp_part, *omax_part, *tmax_part, *pgroup, *tile_max, *upd;
+    void *scratch, *onum, *totT, *pp, *pp_part, *omax_part, *tmax_part, *pgroup, *tile_max, *upd;
     size_t bytes;
 };
 
 struct BatchShape {
-    int TR, TC, nRT, nCT, G, ntiles;
+    int nRT, G, ntiles, chunk;
 };
 
-inline BatchShape batch_shape(int W, int M, int b, int H, int Wc) {
+// Positions per chunk (PTY_BATCH_CHUNK overrides; default: the whole batch)
+inline int batch_chunk(int b) {
+    const int c = env_int("PTY_BATCH_CHUNK", 0);
+    return c > 0 ? std::min(c, b) : b;
+}
+
+template <int W> inline int k4_groups(int chunk) {
+    const int g = env_int("PTY_K4_GROUPS", 0);
+    if (g > 0) return std::min(g, chunk);
+    const int want = 24 * sm_count();                         // K4 team tasks (x modes) in flight
+    return std::max(1, std::min(chunk, (want + W / 4 - 1) / (W / 4)));
+}
+
+inline BatchShape batch_shape(int W, int b, int H, int Wc, int G) {
     BatchShape s;
-    s.TR = 1;
-    while (s.TR < W && s.TR * 2 * M <= 16) s.TR *= 2;         // <= 16 lines per row item
-    s.TC = 4;                                                 // err_part is [N][W/4][3]
-    s.nRT = W / s.TR;
-    s.nCT = W / s.TC;
-    const int want = 8 * sm_count();
-    s.G = std::max(1, std::min(b, (want + s.nRT - 1) / s.nRT));
+    s.chunk = batch_chunk(b);
+    s.nRT = W / 4;                                            // pp_part: 4-row tiles
+    s.G = G;
     s.ntiles = ((H + kObjTile - 1) / kObjTile) * ((Wc + kObjTile - 1) / kObjTile);
     return s;
 }
 
 template <typename T>
-inline BatchLayout carve_batch(void* ws, int W, int M, int b, int H, int Wc, const BatchShape& sh, bool upd) {
+inline BatchLayout carve_batch(void* ws, int W, int M, int b, const BatchShape& sh, int H, int Wc, bool upd) {
     Carver c(ws);
     BatchLayout L{};
     const size_t WW = (size_t)W * W;
     L.anchors = c.take<int>((size_t)b * 2 * sizeof(int));
-    L.scratch = c.take<void>((size_t)b * M * WW * sizeof(cplx<T>));
-    L.onum = c.take<void>((size_t)b * WW * sizeof(cplx<T>));
+    L.scratch = c.take<void>((size_t)sh.chunk * M * WW * sizeof(cplx<T>));
+    L.onum = c.take<void>((size_t)sh.chunk * M * WW * sizeof(cplx<T>));
+    L.totT = c.take<void>((size_t)sh.chunk * WW * sizeof(T));
     L.pp = c.take<void>(WW * sizeof(T));
     L.pp_part = c.take<void>((size_t)sh.nRT * sizeof(T));
-    L.omax_part = c.take<void>((size_t)b * sh.nRT * sizeof(T));
-    L.tmax_part = c.take<void>((size_t)b * sh.nCT * sizeof(T));
+    L.omax_part = c.take<void>((size_t)sh.chunk * (W / 4) * sizeof(T));
+    L.tmax_part = c.take<void>((size_t)sh.chunk * W * sizeof(T));
     L.pgroup = c.take<void>((size_t)sh.G * (2 * M + 1) * WW * sizeof(T));
     L.tile_max = c.take<void>((size_t)sh.ntiles * sizeof(T));
     L.upd = upd ? c.take<void>((size_t)H * Wc * sizeof(cplx<T>)) : nullptr;
@@ -52,26 +62,24 @@ inline BatchLayout carve_batch(void* ws, int W, int M, int b, int H, int Wc, con
 template <typename T, int W>
 int fill_batch(const PtyBatchArgs* a, BatchDev& P, BatchShape& sh, cudaStream_t st) {
     const int M = a->modes, b = a->n_batch;
-    sh = batch_shape(W, M, b, a->H, a->Wc);
+    sh = batch_shape(W, b, a->H, a->Wc, k4_groups<W>(batch_chunk(b)));
     const bool upd = a->sense == PTY_SENSE_XCORR_A;
-    BatchLayout L = carve_batch<T>(a->workspace, W, M, b, a->H, a->Wc, sh, upd);
+    BatchLayout L = carve_batch<T>(a->workspace, W, M, b, sh, a->H, a->Wc, upd);
     if (!a->workspace || a->workspace_bytes < (int64_t)L.bytes) return PTY_ERR_ARGUMENT;
     P = BatchDev{};
     P.W = W; P.M = M; P.N = a->n_positions; P.b = b;
-    P.TR = sh.TR; P.TC = sh.TC; P.nRT = sh.nRT; P.nCT = sh.nCT; P.G = sh.G;
-    P.lgTR = 0; while ((1 << P.lgTR) < sh.TR) ++P.lgTR;
-    P.lgTC = 0; while ((1 << P.lgTC) < sh.TC) ++P.lgTC;
+    P.TR = 4; P.lgTR = 2; P.nRT = sh.nRT; P.G = sh.G;
     P.obj = a->obj; P.H = a->H; P.Wc = a->Wc; P.r0 = a->r0; P.c0 = a->c0;
-    P.probes = a->probes; P.patterns = a->patterns; P.positions = a->positions;
+    P.probes = a->probes; P.patterns = a->patterns; P.patternsT = a->patterns_t; P.positions = a->positions;
     P.batch = a->batch; P.visit0 = a->visit0;
     P.alpha_o = a->alpha_obj; P.alpha_p = a->alpha_probe; P.beta = a->beta; P.gamma = a->gamma;
     P.eps_rel = a->epsilon_rel;
     P.update_probe = a->update_probe; P.track_mod = a->track_modulus; P.sense = a->sense;
     P.stage = a->stage; P.obj_acc = a->obj_acc; P.probe_acc = a->probe_acc;
     P.err_part = a->err_part; P.status = a->status;
-    P.anchors = L.anchors; P.scratch = L.scratch; P.onum = L.onum; P.pp = L.pp; P.pp_part = L.pp_part;
-    P.omax_part = L.omax_part; P.tmax_part = L.tmax_part; P.pgroup = L.pgroup; P.tile_max = L.tile_max;
-    P.upd = L.upd;
+    P.anchors = L.anchors; P.scratch = L.scratch; P.onum = L.onum; P.totT = L.totT; P.pp = L.pp;
+    P.pp_part = L.pp_part; P.omax_part = L.omax_part; P.tmax_part = L.tmax_part; P.pgroup = L.pgroup;
+    P.tile_max = L.tile_max; P.upd = L.upd;
     P.twiddles = twiddles<T, W>(st);
     if (!P.twiddles) return PTY_ERR_CUDA;
     return PTY_OK;
@@ -82,35 +90,63 @@ template <typename K> inline int set_smem(K kern, size_t bytes) {
                ? PTY_OK : PTY_ERR_CUDA;
 }
 
+// persistent grid: every resident CTA slot, capped by the task count
+template <typename K> inline int persistent_grid(K kern, int threads, size_t smem, long tasks_ctas) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+    const long cap = (long)std::max(1, per_sm) * sm_count();
+    return (int)std::max(1L, std::min(cap, tasks_ctas));
+}
+
 template <typename T, int W>
 int run_batch_contrib(const PtyBatchArgs* a, cudaStream_t st) {
     BatchDev P;
     BatchShape sh;
     int rc = fill_batch<T, W>(a, P, sh, st);
     if (rc) return rc;
+    if (!a->patterns_t) return PTY_ERR_ARGUMENT;
     const int M = a->modes, b = a->n_batch;
-    constexpr int LS = line_stride<W>();
-    const size_t fix = (size_t)W * sizeof(cplx<T>) + 64 * sizeof(double);
-    const size_t s_rows = fix + (size_t)sh.TR * M * LS * sizeof(cplx<T>);
-    const size_t s_cols = fix + (size_t)sh.TC * M * LS * sizeof(cplx<T>);
-    const size_t s_inv = s_rows + (size_t)M * sh.TR * W * sizeof(cplx<T>) + (size_t)sh.TR * W * sizeof(T);
-    const size_t s_gather = (size_t)b * sizeof(int);
-    if (s_gather > max_dyn_smem()) return PTY_ERR_ARGUMENT;      // batch too large for one gather list
-    if ((rc = set_smem(bk_rows_fwd<T, W>, s_rows)) || (rc = set_smem(bk_cols_fwd<T, W>, s_cols)) ||
-        (rc = set_smem(bk_cols_mod<T, W>, s_cols)) || (rc = set_smem(bk_rows_inv<T, W>, s_inv)) ||
+    constexpr int B = Shape<W>::B, TEAM = 4 * B, NTEAM = kLineThreads / TEAM, XS = xch_size<W>();
+    constexpr int LS4 = team_line_stride<W>();
+    using C = cplx<T>;
+    const size_t s_k1 = W * sizeof(C) + (kLineThreads / B) * XS * sizeof(C) + NTEAM * W * 5 * sizeof(C) + 64 * sizeof(T);
+    const size_t s_k23 = W * sizeof(C) + (kLineThreads / B) * XS * sizeof(C);
+    const size_t s_k4 = W * sizeof(C) + 4 * LS4 * sizeof(C) + 4 * W * sizeof(C) + 4 * W * sizeof(T);
+    const size_t s_gather = (size_t)sh.chunk * sizeof(int);
+    if (s_gather > max_dyn_smem() || s_k4 > max_dyn_smem()) return PTY_ERR_ARGUMENT;
+    if ((rc = set_smem(bk_rows_fwd<T, W>, s_k1)) || (rc = set_smem(bk_cols_fwd<T, W>, s_k23)) ||
+        (rc = set_smem(bk_cols_mod<T, W>, s_k23)) || (rc = set_smem(bk_rows_inv<T, W>, s_k4)) ||
         (rc = set_smem(bk_obj_gather<T, W>, s_gather)))
         return rc;
     const size_t HW = (size_t)a->H * a->Wc, WW = (size_t)W * W;
     cudaMemsetAsync(a->obj_acc, 0, 3 * HW * sizeof(T), st);
     cudaMemsetAsync(a->probe_acc, 0, (size_t)(2 * M + 1) * WW * sizeof(T), st);
     bk_probe_power<T, W><<<std::max(sh.nRT, (b + kBatThreads - 1) / kBatThreads), kBatThreads, 0, st>>>(P);
-    bk_rows_fwd<T, W><<<b * sh.nRT, kBatThreads, s_rows, st>>>(P);
-    bk_cols_fwd<T, W><<<b * sh.nCT, kBatThreads, s_cols, st>>>(P);
-    bk_cols_mod<T, W><<<b * sh.nCT, kBatThreads, s_cols, st>>>(P);
-    bk_rows_inv<T, W><<<sh.nRT * sh.G, kBatThreads, s_inv, st>>>(P);
+    int launches = 1;
+    for (int off = 0; off < b; off += sh.chunk) {   // the batch in chunks, in order
+        BatchDev Q = P;
+        Q.b = std::min(sh.chunk, b - off);
+        Q.batch = P.batch + off;
+        Q.anchors = P.anchors + 2 * off;
+        Q.visit0 = P.visit0 + off;
+        Q.accumulate = off > 0;
+        Q.G = std::min(sh.G, Q.b);
+        const long t1 = (long)Q.b * M * (W / 4), t23 = (long)Q.b * W;
+        bk_rows_fwd<T, W><<<persistent_grid(bk_rows_fwd<T, W>, kLineThreads, s_k1, (t1 + NTEAM - 1) / NTEAM),
+                            kLineThreads, s_k1, st>>>(Q);
+        bk_cols_fwd<T, W><<<persistent_grid(bk_cols_fwd<T, W>, kLineThreads, s_k23, (t23 * B + kLineThreads - 1) / kLineThreads),
+                            kLineThreads, s_k23, st>>>(Q);
+        bk_cols_mod<T, W><<<persistent_grid(bk_cols_mod<T, W>, kLineThreads, s_k23, (t23 * B + kLineThreads - 1) / kLineThreads),
+                            kLineThreads, s_k23, st>>>(Q);
+        // a short last chunk has fewer groups: the missing groups' partials
+        // keep their earlier values (bk_probe_reduce sums P.G groups)
+        bk_rows_inv<T, W><<<persistent_grid(bk_rows_inv<T, W>, TEAM, s_k4, (long)(W / 4) * M * Q.G), TEAM, s_k4, st>>>(Q);
+        bk_obj_gather<T, W><<<sh.ntiles, 256, s_gather, st>>>(Q);
+        launches += 5;
+    }
+    P.G = std::min(sh.G, b);
     bk_probe_reduce<T, W><<<std::min<size_t>(4096, ((2 * M + 1) * WW + 255) / 256), 256, 0, st>>>(P);
-    bk_obj_gather<T, W><<<sh.ntiles, 256, s_gather, st>>>(P);
-    count(7);
+    count(launches + 1);
     return last_status();
 }
 
@@ -138,8 +174,8 @@ int run_batch_apply(const PtyBatchArgs* a, cudaStream_t st) {
 
 template <typename T, int W>
 int64_t batch_workspace(int M, int b, int H, int Wc, bool upd) {
-    BatchShape sh = batch_shape(W, M, b, H, Wc);
-    return (int64_t)carve_batch<T>(nullptr, W, M, b, H, Wc, sh, upd).bytes;
+    BatchShape sh = batch_shape(W, b, H, Wc, k4_groups<W>(batch_chunk(b)));
+    return (int64_t)carve_batch<T>(nullptr, W, M, b, sh, H, Wc, upd).bytes;
 }
 
 }  // namespace pty

@@ -137,8 +137,8 @@ int pty_device_info(int32_t* sm, int32_t* coop, int32_t* major, int32_t* minor) 
 
 int64_t pty_sweep_workspace_bytes(int32_t dtype, int32_t W, int32_t M, int32_t N, int32_t S) {
     if (!valid_window(W) || M < 1 || M > kMaxModes || N < 1 || S < 1 || S > kMaxSlots) return -1;
-    if (dtype == PTY_DTYPE_C64) return (int64_t)carve_sweep<float>(nullptr, W, M, N, S).bytes;
-    if (dtype == PTY_DTYPE_C128) return (int64_t)carve_sweep<double>(nullptr, W, M, N, S).bytes;
+    if (dtype == PTY_DTYPE_C64) return (int64_t)sweep_workspace<float>(W, M, N, S);
+    if (dtype == PTY_DTYPE_C128) return (int64_t)sweep_workspace<double>(W, M, N, S);
     return -1;
 }
 
@@ -342,7 +342,7 @@ int64_t pty_batch_workspace_bytes(int32_t dtype, int32_t W, int32_t M, int32_t b
 
 static int batch_check(const PtyBatchArgs* a) {
     if (!a || !valid_window(a->window) || a->modes < 1 || a->modes > kMaxBatchModes || a->n_batch < 1 ||
-        !a->obj || !a->probes || !a->patterns || !a->positions || !a->batch || !a->obj_acc ||
+        !a->obj || !a->probes || !a->patterns || !a->patterns_t || !a->positions || !a->batch || !a->obj_acc ||
         !a->probe_acc || !a->err_part || !a->status || a->H < a->window || a->Wc < a->window ||
         a->visit0 < 0 || a->visit0 + a->n_batch > a->n_positions)
         return PTY_ERR_ARGUMENT;
@@ -372,8 +372,13 @@ int pty_batch_finalize(const double* err_part, int32_t n_visits, int32_t W, doub
     if (!err_part || !err_out || n_visits < 1 || !valid_window(W)) return PTY_ERR_ARGUMENT;
     ErrOut outs{};
     outs.p[0] = err_out;
-    sweep_finalize_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(err_part, n_visits, W / 4, 1, outs);
-    count();
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    double* vs = nullptr;
+    if (cudaMallocAsync(&vs, (size_t)n_visits * 3 * sizeof(double), st) != cudaSuccess) return PTY_ERR_CUDA;
+    err_visit_kernel<<<n_visits, 256, 0, st>>>(err_part, W, vs);
+    err_slot_kernel<<<1, 256, 0, st>>>(vs, n_visits, 1, outs);
+    cudaFreeAsync(vs, st);
+    count(2);
     return last_status();
 }
 

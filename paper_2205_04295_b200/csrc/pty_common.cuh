@@ -102,6 +102,20 @@ struct GridBarrier {
     }
 };
 
+// cp.async (LDGSTS): global -> shared without register staging, so a thread
+// can have all its tile elements in flight at once.  Element sizes 4/8/16 B.
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    if constexpr (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(s), "l"(gmem), "n"(BYTES) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
 // (-1)^(r+c) checkerboard: the fftshift/ifftshift pair of a centered DFT of
 // even size becomes a sign flip on load and store.
 template <typename T> __device__ __forceinline__ T checker(int r, int c) {

@@ -149,6 +149,45 @@ __device__ __forceinline__ void line_fft(cplx<T>* line, const cplx<T>* tw, int b
     __syncwarp(mask);
 }
 
+// Fused-I/O line FFT by a group of B threads.  Stage 1 takes its A inputs from
+// load(n, a) with n = B*a + b (for fixed a the group reads B consecutive
+// elements: coalesced from global memory); stage 2 hands each output to
+// store(k, slot, value) with k = b + B*i + A*k2 and slot = i*B + k2 (a thread's
+// output set is fixed, so per-thread accumulators can be indexed by slot).
+// xch: the group's exchange buffer, A*(B+1) complex, may alias the input when
+// the input is shared memory (all stage-1 reads precede the first write).
+template <typename T, int W, bool INV, typename LD, typename ST>
+__device__ __forceinline__ void group_fft(cplx<T>* xch, const cplx<T>* tw, int b, unsigned mask, LD&& load,
+                                          ST&& store) {
+    constexpr int A = Shape<W>::A, B = Shape<W>::B, Q = A / B;
+    cplx<T> v[A];
+#pragma unroll
+    for (int a = 0; a < A; ++a) v[a] = load(B * a + b, a);
+    DFT<T, A, INV>::run(v);
+#pragma unroll
+    for (int k1 = 1; k1 < A; ++k1) {
+        const cplx<T> w = tw[k1 * B + b];
+        v[k1] = INV ? mulc(v[k1], w) : v[k1] * w;
+    }
+    __syncwarp(mask);
+#pragma unroll
+    for (int k1 = 0; k1 < A; ++k1) xch[k1 * (B + 1) + b] = v[k1];
+    __syncwarp(mask);
+#pragma unroll
+    for (int i = 0; i < Q; ++i)
+#pragma unroll
+        for (int j = 0; j < B; ++j) v[i * B + j] = xch[(b + B * i) * (B + 1) + j];
+    __syncwarp(mask);
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+        DFT<T, B, INV>::run(&v[i * B]);
+#pragma unroll
+        for (int k2 = 0; k2 < B; ++k2) store(b + B * i + A * k2, i * B + k2, v[i * B + k2]);
+    }
+}
+
+template <int W> __host__ __device__ constexpr int xch_size() { return Shape<W>::A * (Shape<W>::B + 1); }
+
 // Run `nlines` line FFTs (lines at base + l * stride) with every line group of
 // the CTA.  Caller synchronises the block before and after.
 template <typename T, int W, bool INV>

@@ -17,13 +17,13 @@
 // separated by a software grid barrier.  The centered DFT of fields.py:71-84 is
 // C * DFT(C * x) / W for even W, so no fftshift is materialised.
 #pragma once
-#include "pty_fft.cuh"
+#include "pty_tasks.cuh"
 #include "../../include/ptycho_b200.h"
 
 namespace pty {
 
 constexpr int kSweepThreads = 256;
-constexpr int kSweepMinCtasPerSm = 2;
+constexpr int kSweepMaxCtasPerSm = 2;
 constexpr int kMaxSlots = 24;
 constexpr int kMaxModes = 8;
 
@@ -32,6 +32,7 @@ struct SlotDev {
     int H, Wc, r0, c0;
     void* probes;
     const void* patterns;
+    const void* patterns_t;       // [N][W][W] each pattern transposed
     const double* positions;
     const int* order;
     void* stage;
@@ -41,43 +42,39 @@ struct SlotDev {
 
 struct SweepDev {
     int W, M, N, nslots;
-    int TR, TC, nRT, nCT, K;      // row tile, col tile, tile counts, col items held per CTA
-    int lgTR, lgTC;               // log2 of the (power-of-two) tile sizes
     double alpha_o, alpha_p, beta, gamma, eps_rel;
     int update_probe, track_mod, sense;
     // workspace
     unsigned int* barrier;
     int* anchors;                 // [nslots][N][2]
-    void* scratch;                // [nslots][M][W][W] complex
-    void* omax_part;              // [nslots][nRT] real
-    void* peak_part;              // [2][nslots][nRT] real
-    void* tmax_part;              // [nslots][nCT] real
-    double* err_part;             // [nslots][N][nCT][3] per-visit error partials
+    void* scratch;                // [nslots][M][W][W] complex, transposed after the row pass
+    void* totT;                   // [nslots][W][W] real
+    void* omax_part;              // [nslots][W/4] real
+    void* peak_part;              // [2][nslots][W/4] real
+    void* tmax_part;              // [nslots][W] real
+    double* err_part;             // [nslots][N][W][3] per-visit, per-column error terms
     const void* twiddles;         // [W] complex, global
     unsigned long long* timeline; // debug: [steps][5][gridDim] globaltimer stamps or null
     int timeline_steps;
     SlotDev slot[kMaxSlots];
 };
 
-// shared-memory carve-up (bytes): twiddles | reduction scratch | tile region
+// shared-memory carve-up (bytes): twiddles | reduction scratch | phase region
 template <typename T, int W>
 __host__ __device__ constexpr size_t sweep_smem_fixed() {
     return (size_t)W * sizeof(cplx<T>) + 64 * sizeof(double);
 }
+// phase region: max over P1 (group exchange + team transpose tiles), P2/P3
+// (group exchange) and P4 (team lines + per-team accumulators)
 template <typename T, int W>
-__host__ __device__ inline size_t sweep_smem_rows(int TR, int M) {
-    return (size_t)TR * M * line_stride<W>() * sizeof(cplx<T>);
-}
-template <typename T, int W>
-__host__ __device__ inline size_t sweep_smem_cols(int TC, int M, int K) {
-    return (size_t)K * M * TC * line_stride<W>() * sizeof(cplx<T>);
-}
-
-template <typename T>
-__device__ __forceinline__ T reduce_max_global(const T* p, int n) {
-    T m = T(0);
-    for (int i = 0; i < n; ++i) m = fmax(m, p[i]);
-    return m;
+__host__ __device__ constexpr size_t sweep_smem_phase(int threads) {
+    constexpr int B = Shape<W>::B, TEAM = 4 * B, XS = xch_size<W>(), LS4 = team_line_stride<W>();
+    const int ngroups = threads / B, nteams = threads / TEAM;
+    const size_t p1 = (size_t)ngroups * XS * sizeof(cplx<T>) + (size_t)nteams * W * 5 * sizeof(cplx<T>) +
+                      (size_t)nteams * 4 * sizeof(T);
+    const size_t p4 = (size_t)nteams * 4 * LS4 * sizeof(cplx<T>) +
+                      (size_t)nteams * 4 * W * (sizeof(cplx<T>) + 2 * sizeof(T)) + (size_t)nteams * 4 * sizeof(T);
+    return p1 > p4 ? p1 : p4;
 }
 
 // Prefetch [base, base + bytes) into L2 (or L1 when to_l1), one request per
@@ -125,338 +122,44 @@ __device__ __forceinline__ T cta_max_of(const T* p, int n, T* cell) {
 // phase body; they are inlined (non-inlined member calls spill the CTA state
 // to local memory, measured 2x slower).
 template <typename T, int W>
-struct SweepCta {
+__global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kernel(const __grid_constant__ SweepDev P) {
     using C = cplx<T>;
-    static constexpr int LS = line_stride<W>();
-    const SweepDev& P;
-    C* tw;
-    T* red;
-    C* tile;
-    int* s_dead;
-    int* s_j;
-    int* s_ar;
-    int* s_ac;
-    T* cellT;
-    C* scratch;
-    T* omax_part;
-    T* peak_part;
-    T* tmax_part;
-    int tid, NT, M, N, S;
-    size_t WW;
-    T invW2, alpha_o, alpha_p, beta, gamma, eps_rel;
-
-    __device__ __forceinline__ void phase1(int step) {
-    // ------------------------------------------------------------ P1 rows
-    for (int item = blockIdx.x; item < S * P.nRT; item += gridDim.x) {
-        const int s = item / P.nRT, rt = item % P.nRT;
-        const SlotDev& sl = P.slot[s];
-        if (s_dead[s]) continue;
-        const int ar = s_ar[s], ac = s_ac[s];
-        const C* obj = reinterpret_cast<const C*>(sl.obj);
-        const C* probes = reinterpret_cast<const C*>(sl.probes);
-        // the pattern rows P3 will read: HBM -> L2 while P1/P2 run
-        prefetch_span(reinterpret_cast<const T*>(sl.patterns) + (size_t)s_j[s] * WW + (size_t)rt * P.TR * W,
-                      (size_t)P.TR * W * sizeof(T), false);
-        T om = T(0);
-        constexpr int U = 8;
-        const int nel = P.TR * M * W;          // element = (row, mode, column)
-        batched<U>(nel, [&](int i0) {
-            C o[U], p[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int i = i0 + u * NT;
-                if (i < nel) {
-                    const int l = i / W, c = i % W, m = l >> P.lgTR, r = l & (P.TR - 1), rr = rt * P.TR + r;
-                    o[u] = obj[(size_t)(ar + rr) * sl.Wc + ac + c];
-                    p[u] = probes[m * WW + (size_t)rr * W + c];
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int i = i0 + u * NT;
-                if (i < nel) {
-                    const int l = i / W, c = i % W, m = l >> P.lgTR, rr = rt * P.TR + (l & (P.TR - 1));
-                    if (m == 0) om = fmax(om, norm2(o[u]));
-                    tile[(size_t)l * LS + pad<W>(c)] = scale(p[u] * o[u], checker<T>(rr, c));
-                }
-            }
-        });
-        om = block_max(om, red);
-        if (tid == 0) omax_part[(size_t)s * P.nRT + rt] = om;
-        __syncthreads();
-        lines_fft<T, W, false>(tile, P.TR * M, LS, tw);
-        __syncthreads();
-        C* scr = scratch + (size_t)s * M * WW;
-        for (int i = tid; i < P.TR * M * W; i += NT) {   // lines are mode-major: contiguous rows
-            const int l = i / W, c = i % W;
-            scr[(l >> P.lgTR) * WW + (size_t)(rt * P.TR + (l & (P.TR - 1))) * W + c] = tile[(size_t)l * LS + pad<W>(c)];
-        }
-        __syncthreads();
-    }
-    }
-
-    __device__ __forceinline__ void phase2(int step) {
-    // ------------------------------------------------- P2 cols (forward)
-    int held = 0;
-    for (int item = blockIdx.x; item < S * P.nCT; item += gridDim.x, ++held) {
-        const int s = item / P.nCT, ct = item % P.nCT;
-        if (s_dead[s]) continue;
-        C* my = tile + (size_t)held * M * P.TC * LS;
-        const C* scr = scratch + (size_t)s * M * WW;
-        {
-            constexpr int U = 8;
-            const int nel = M * W * P.TC;
-            batched<U>(nel, [&](int i0) {
-                C v[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int i = i0 + u * NT;
-                    if (i < nel) {
-                        const int rem = i & ((W << P.lgTC) - 1), m = i >> (P.lgTC + Log2<W>::value);
-                        v[u] = scr[m * WW + (size_t)(rem >> P.lgTC) * W + ct * P.TC + (rem & (P.TC - 1))];
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int i = i0 + u * NT;
-                    if (i < nel) {
-                        const int rem = i & ((W << P.lgTC) - 1), m = i >> (P.lgTC + Log2<W>::value);
-                        my[(size_t)((m << P.lgTC) + (rem & (P.TC - 1))) * LS + pad<W>(rem >> P.lgTC)] = v[u];
-                    }
-                }
-            });
-        }
-        __syncthreads();
-        lines_fft<T, W, false>(my, M * P.TC, LS, tw);
-        __syncthreads();
-        T tm = T(0);
-        for (int i = tid; i < W * P.TC; i += NT) {
-            const int cc = i / W, r = i % W;   // W is a compile-time power of two
-            T tot = T(0);
-            for (int m = 0; m < M; ++m) tot += norm2(my[(size_t)(m * P.TC + cc) * LS + pad<W>(r)]) * invW2;
-            tm = fmax(tm, tot);
-        }
-        tm = block_max(tm, red);
-        if (tid == 0) tmax_part[(size_t)s * P.nCT + ct] = tm;
-    }
-    }
-
-    __device__ __forceinline__ void phase3(int step) {
-    // ------------------------------------- P3 modulus + cols (inverse)
-    int held = 0;
-    for (int item = blockIdx.x; item < S * P.nCT; item += gridDim.x, ++held) {
-        const int s = item / P.nCT, ct = item % P.nCT;
-        const SlotDev& sl = P.slot[s];
-        if (s_dead[s]) continue;
-        C* my = tile + (size_t)held * M * P.TC * LS;
-        const int j = s_j[s];
-        const T tmax = cta_max_of(tmax_part + (size_t)s * P.nCT, P.nCT, cellT);
-        const T eps = eps_rel * fmax(tmax, real_limits<T>::tiny());
-        const T* I = reinterpret_cast<const T*>(sl.patterns) + (size_t)j * WW;
-        C* stg = P.sense == PTY_SENSE_XCORR_B ? reinterpret_cast<C*>(sl.stage) + (size_t)j * 2 * WW : nullptr;
-        double enum_ = 0.0, eden = 0.0;
-        T worst = T(0);
-        constexpr int UI = 8;
-        const int npx = W * P.TC;
-        batched<UI>(npx, [&](int i0) {
-          T Ib[UI];
-#pragma unroll
-          for (int u = 0; u < UI; ++u) {
-            const int i = i0 + u * NT;
-            if (i < npx) Ib[u] = I[(size_t)(i >> P.lgTC) * W + ct * P.TC + (i & (P.TC - 1))];
-          }
-#pragma unroll
-          for (int u = 0; u < UI; ++u) {
-            const int i = i0 + u * NT;
-            if (i >= npx) continue;
-            const int r = i >> P.lgTC, cc = i & (P.TC - 1), c = ct * P.TC + cc;
-            T tot = T(0);
-            for (int m = 0; m < M; ++m) tot += norm2(my[(size_t)(m * P.TC + cc) * LS + pad<W>(r)]) * invW2;
-            const T Iv = Ib[u];
-            const T sI = sqrt_rn(Iv);
-            const T sc = sI / sqrt_rn(tot + eps);
-            const T d = sqrt_rn(tot) - sI;
-            enum_ += (double)(d * d);
-            eden += (double)Iv;
-            T after = T(0);
-            for (int m = 0; m < M; ++m) {
-                C& a = my[(size_t)(m * P.TC + cc) * LS + pad<W>(r)];
-                a = scale(a, sc);
-                after += norm2(a) * invW2;
-            }
-            if (P.track_mod && tot > T(1e-3) * tmax) {
-                worst = fmax(worst, fabs(after - Iv) / fmax(Iv, real_limits<T>::tiny()));
-            }
-            if (stg) {
-                stg[(size_t)r * W + c] = C{tot, T(0)};
-                stg[WW + (size_t)r * W + c] = C{Iv, T(0)};
-            }
-          }
-        });
-        __syncthreads();
-        lines_fft<T, W, true>(my, M * P.TC, LS, tw);
-        __syncthreads();
-        enum_ = block_sum(enum_, reinterpret_cast<double*>(red));
-        eden = block_sum(eden, reinterpret_cast<double*>(red));
-        worst = block_max(worst, red);
-        if (tid == 0) {
-            double* e = P.err_part + (((size_t)s * N + step) * P.nCT + ct) * 3;
-            e[0] = enum_;
-            e[1] = eden;
-            e[2] = (double)worst;
-        }
-        C* scr = scratch + (size_t)s * M * WW;
-        for (int i = tid; i < M * W * P.TC; i += NT) {
-            const int rem = i & ((W << P.lgTC) - 1), m = i >> (P.lgTC + Log2<W>::value);
-            const int r = rem >> P.lgTC, cc = rem & (P.TC - 1);
-            scr[m * WW + (size_t)r * W + ct * P.TC + cc] = my[(size_t)((m << P.lgTC) + cc) * LS + pad<W>(r)];
-        }
-        __syncthreads();
-    }
-    }
-
-    __device__ __forceinline__ void phase4(int step) {
-    // ------------------------------------------ P4 rows (inverse) + update
-    for (int item = blockIdx.x; item < S * P.nRT; item += gridDim.x) {
-        const int s = item / P.nRT, rt = item % P.nRT;
-        const SlotDev& sl = P.slot[s];
-        if (s_dead[s]) continue;
-        const int j = s_j[s];
-        const T peak = cta_max_of(peak_part + ((size_t)(step & 1) * S + s) * P.nRT, P.nRT, cellT);
-        const T omax = cta_max_of(omax_part + (size_t)s * P.nRT, P.nRT, cellT);
-        if (peak == T(0)) {                      // engine.py:132-134
-            if (tid == 0) atomicOr(sl.status, PTY_ERR_PROBE_ZERO);
-            continue;
-        }
-        if (P.update_probe && omax == T(0)) {    // engine.py:145-147
-            if (tid == 0) atomicOr(sl.status, PTY_ERR_OBJECT_ZERO);
-            continue;
-        }
-        const int ar = s_ar[s], ac = s_ac[s];
-        {   // obj / probe rows of the update: into L1 while the inverse DFTs run
-            const bool l1 = (size_t)P.TR * (M + 1) * W * sizeof(C) <= 16 * 1024;
-            for (int r = 0; r < P.TR; ++r) {
-                const int rr = rt * P.TR + r;
-                prefetch_span(reinterpret_cast<const C*>(sl.obj) + (size_t)(ar + rr) * sl.Wc + ac, W * sizeof(C), l1);
-                for (int m = 0; m < M; ++m)
-                    prefetch_span(reinterpret_cast<const C*>(sl.probes) + m * WW + (size_t)rr * W, W * sizeof(C), l1);
-            }
-        }
-        const C* scr = scratch + (size_t)s * M * WW;
-        {
-            constexpr int U = 8;
-            const int nel = P.TR * M * W;
-            batched<U>(nel, [&](int i0) {
-                C v[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int i = i0 + u * NT;
-                    if (i < nel) {
-                        const int l = i / W, c = i % W;
-                        v[u] = scr[(l >> P.lgTR) * WW + (size_t)(rt * P.TR + (l & (P.TR - 1))) * W + c];
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int i = i0 + u * NT;
-                    if (i < nel) tile[(size_t)(i / W) * LS + pad<W>(i % W)] = v[u];
-                }
-            });
-        }
-        __syncthreads();
-        lines_fft<T, W, true>(tile, P.TR * M, LS, tw);
-        __syncthreads();
-        C* obj = reinterpret_cast<C*>(sl.obj);
-        C* probes = reinterpret_cast<C*>(sl.probes);
-        C* stg = P.sense == PTY_SENSE_XCORR_A ? reinterpret_cast<C*>(sl.stage) + (size_t)j * 2 * WW : nullptr;
-        const T dmax_o = gamma * peak + (T(1) - gamma) * peak;   // = max of the object denominator
-        const T dmax_p = beta * omax + (T(1) - beta) * omax;
-        T pk = T(0);
-        for (int i = tid; i < P.TR * W; i += NT) {
-            const int r = i / W, c = i % W, rr = rt * P.TR + r;
-            const size_t oi = (size_t)(ar + rr) * sl.Wc + ac + c;
-            const C o = obj[oi];
-            const T sg = checker<T>(rr, c) * invW2;
-            C numer{T(0), T(0)};
-            T pp = T(0);
-            for (int m = 0; m < M; ++m) {
-                const C pv = probes[m * WW + (size_t)rr * W + c];
-                const C psi = scale(tile[(size_t)((m << P.lgTR) + r) * LS + pad<W>(c)], sg);
-                numer = numer + mulc(psi - pv * o, pv);
-                pp += norm2(pv);
-            }
-            T den = gamma * peak + (T(1) - gamma) * pp;
-            den = den + eps_rel * dmax_o;
-            const C no = o + divr(scale(numer, alpha_o), den);
-            obj[oi] = o + (no - o);                              // paste_add_inplace
-            if (stg) {
-                stg[(size_t)rr * W + c] = o;
-                stg[WW + (size_t)rr * W + c] = no;
-            }
-            if (P.update_probe) {
-                const T op = norm2(o);
-                T dp = beta * omax + (T(1) - beta) * op;
-                dp = dp + eps_rel * dmax_p;
-                T npp = T(0);
-                for (int m = 0; m < M; ++m) {   // pre-update probes and o_j (engine.py:218-223)
-                    const size_t pi = m * WW + (size_t)rr * W + c;
-                    const C pv = probes[pi];
-                    const C psi = scale(tile[(size_t)((m << P.lgTR) + r) * LS + pad<W>(c)], sg);
-                    const C np_ = pv + divr(mulc(scale(psi - pv * o, alpha_p), o), dp);
-                    probes[pi] = np_;
-                    npp += norm2(np_);
-                }
-                pk = fmax(pk, npp);
-            } else {
-                pk = fmax(pk, pp);
-            }
-        }
-        pk = block_max(pk, red);
-        if (tid == 0) peak_part[((size_t)((step + 1) & 1) * S + s) * P.nRT + rt] = pk;
-        __syncthreads();
-    }
-    }
-};
-
-template <typename T, int W>
-__global__ void __launch_bounds__(kSweepThreads, kSweepMinCtasPerSm) sweep_kernel(const __grid_constant__ SweepDev P) {
-    using C = cplx<T>;
+    constexpr int B = Shape<W>::B, TEAM = 4 * B, XS = xch_size<W>(), LS4 = team_line_stride<W>();
+    constexpr int NTEAM = kSweepThreads / TEAM, NGRP = kSweepThreads / B;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // per-step snapshot of every slot: dead flag, position index, anchor
     __shared__ int s_dead[kMaxSlots], s_j[kMaxSlots], s_ar[kMaxSlots], s_ac[kMaxSlots];
-    __shared__ double s_cell[2];
-    SweepCta<T, W> X{P};
-    X.tw = reinterpret_cast<C*>(smem_raw);
-    X.red = reinterpret_cast<T*>(smem_raw + (size_t)W * sizeof(C));
-    X.tile = reinterpret_cast<C*>(smem_raw + sweep_smem_fixed<T, W>());
-    X.s_dead = s_dead;
-    X.s_j = s_j;
-    X.s_ar = s_ar;
-    X.s_ac = s_ac;
-    X.cellT = reinterpret_cast<T*>(s_cell);
-    X.scratch = reinterpret_cast<C*>(P.scratch);
-    X.omax_part = reinterpret_cast<T*>(P.omax_part);
-    X.peak_part = reinterpret_cast<T*>(P.peak_part);
-    X.tmax_part = reinterpret_cast<T*>(P.tmax_part);
-    X.tid = threadIdx.x;
-    X.NT = blockDim.x;
-    X.M = P.M;
-    X.N = P.N;
-    X.S = P.nslots;
-    X.WW = (size_t)W * W;
-    X.invW2 = T(1) / (T(W) * T(W));
-    X.alpha_o = T(P.alpha_o);
-    X.alpha_p = T(P.alpha_p);
-    X.beta = T(P.beta);
-    X.gamma = T(P.gamma);
-    X.eps_rel = T(P.eps_rel);
-    const int tid = threadIdx.x, NT = blockDim.x, M = P.M, N = P.N, S = P.nslots;
+    C* tw = reinterpret_cast<C*>(smem_raw);
+    T* red = reinterpret_cast<T*>(smem_raw + (size_t)W * sizeof(C));
+    unsigned char* region = smem_raw + sweep_smem_fixed<T, W>();
+
+    const int tid = threadIdx.x, NT = blockDim.x;
+    const int M = P.M, N = P.N, S = P.nslots;
     const size_t WW = (size_t)W * W;
-    T* red = X.red;
-    T* peak_part = X.peak_part;
+    const int nq = W / 4;
+    const int team = tid / TEAM, tl = tid % TEAM, gi = tl / B, b = tid % B, grp = tid / B;
+    const unsigned gmask = group_mask<W>();
+    const UpdateParams U{P.alpha_o, P.alpha_p, P.beta, P.gamma, P.eps_rel, P.update_probe};
+    C* scratch = reinterpret_cast<C*>(P.scratch);
+    T* totT = reinterpret_cast<T*>(P.totT);
+    T* omax_part = reinterpret_cast<T*>(P.omax_part);
+    T* peak_part = reinterpret_cast<T*>(P.peak_part);
+    T* tmax_part = reinterpret_cast<T*>(P.tmax_part);
+    // phase-region views
+    C* xch = reinterpret_cast<C*>(region) + grp * XS;                          // P1-P3
+    C* tt = reinterpret_cast<C*>(region) + (size_t)NGRP * XS + (size_t)team * W * 5;   // P1
+    T* red4_p1 = reinterpret_cast<T*>(reinterpret_cast<C*>(region) + (size_t)NGRP * XS + (size_t)NTEAM * W * 5) + team * 4;
+    C* lines = reinterpret_cast<C*>(region) + (size_t)team * 4 * LS4;                  // P4
+    C* numer = reinterpret_cast<C*>(region) + (size_t)NTEAM * 4 * LS4 + (size_t)team * 4 * W;
+    T* ppacc = reinterpret_cast<T*>(reinterpret_cast<C*>(region) + (size_t)NTEAM * 4 * LS4 + (size_t)NTEAM * 4 * W) +
+               (size_t)team * 4 * W;
+    T* nppacc = reinterpret_cast<T*>(reinterpret_cast<C*>(region) + (size_t)NTEAM * 4 * LS4 + (size_t)NTEAM * 4 * W) +
+                (size_t)NTEAM * 4 * W + (size_t)team * 4 * W;
+    T* red4_p4 = reinterpret_cast<T*>(reinterpret_cast<C*>(region) + (size_t)NTEAM * 4 * LS4 + (size_t)NTEAM * 4 * W) +
+                 (size_t)2 * NTEAM * 4 * W + team * 4;
 
     GridBarrier bar{P.barrier, 0u};
-    load_twiddles<T, W>(X.tw, reinterpret_cast<const C*>(P.twiddles));
+    load_twiddles<T, W>(tw, reinterpret_cast<const C*>(P.twiddles));
 
     // ---- phase 0: anchors (engine.py:69-70, 192-195) + bounds, initial probe peak
     for (int idx = blockIdx.x * NT + tid; idx < S * N; idx += gridDim.x * NT) {
@@ -469,18 +172,18 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMinCtasPerSm) sweep_kerne
         P.anchors[2 * idx + 1] = ac;
         if (ar < 0 || ac < 0 || ar + W > sl.H || ac + W > sl.Wc) atomicOr(sl.status, PTY_ERR_BOUNDS);
     }
-    for (int item = blockIdx.x; item < S * P.nRT; item += gridDim.x) {
-        const int s = item / P.nRT, rt = item % P.nRT;
+    for (int item = blockIdx.x; item < S * nq; item += gridDim.x) {
+        const int s = item / nq, rq = item % nq;
         const C* probes = reinterpret_cast<const C*>(P.slot[s].probes);
         T pk = T(0);
-        for (int i = tid; i < P.TR * W; i += NT) {
-            const size_t off = (size_t)(rt * P.TR) * W + i;
+        for (int i = tid; i < 4 * W; i += NT) {
+            const size_t off = (size_t)(4 * rq) * W + i;
             T pp = T(0);
             for (int m = 0; m < M; ++m) pp += norm2(probes[m * WW + off]);
             pk = fmax(pk, pp);
         }
         pk = block_max(pk, red);
-        if (tid == 0) peak_part[(size_t)s * P.nRT + rt] = pk;
+        if (tid == 0) peak_part[(size_t)s * nq + rq] = pk;
     }
     bar.sync();
 
@@ -501,40 +204,120 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMinCtasPerSm) sweep_kerne
             s_ac[tid] = P.anchors[2 * (tid * N + j) + 1];
         }
         __syncthreads();
-        X.phase1(step);
+        // ---------------------------------------------------------- P1 rows
+        for (int task = blockIdx.x * NTEAM + team; task < S * M * nq; task += gridDim.x * NTEAM) {
+            const int s = task / (M * nq), m = (task / nq) % M, rq = task % nq;
+            if (s_dead[s]) continue;
+            const SlotDev& sl = P.slot[s];
+            const int j = s_j[s];
+            // this visit's pattern column lines P3 will read: HBM -> L2
+            if (m == 0) {
+                const char* It = reinterpret_cast<const char*>(reinterpret_cast<const T*>(sl.patterns_t) + (size_t)j * WW +
+                                                               (size_t)4 * rq * W);
+                for (int q = tl; q < (int)(4 * W * sizeof(T) / 128); q += TEAM)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(It + q * 128));
+            }
+            C* stg = (P.sense == PTY_SENSE_XCORR_A && m == 0) ? reinterpret_cast<C*>(sl.stage) + (size_t)j * 2 * WW : nullptr;
+            const T om = task_row_fwd<T, W>(tw, xch, tt, red4_p1, team, tl, gi, b, gmask,
+                                            reinterpret_cast<const C*>(sl.obj), sl.Wc, s_ar[s], s_ac[s],
+                                            reinterpret_cast<const C*>(sl.probes), m, rq, scratch + (size_t)s * M * WW, stg);
+            if (m == 0 && tl == 0) omax_part[(size_t)s * nq + rq] = om;
+        }
         stamp(step, 1);
         bar.sync();
-        X.phase2(step);
+        // ------------------------------------------------- P2 cols (forward)
+        for (int task = blockIdx.x * NGRP + grp; task < S * W; task += gridDim.x * NGRP) {
+            const int s = task / W, kc = task % W;
+            if (s_dead[s]) continue;
+            const T tm = task_col_fwd<T, W>(tw, xch, b, gmask, scratch + (size_t)s * M * WW, M, kc, totT + (size_t)s * WW);
+            if (b == 0) tmax_part[(size_t)s * W + kc] = tm;
+        }
         stamp(step, 2);
         bar.sync();
-        X.phase3(step);
+        // ---------------------------------------- P3 modulus + cols (inverse)
+        for (int task = blockIdx.x * NGRP + grp; task < S * W; task += gridDim.x * NGRP) {
+            const int s = task / W, kc = task % W;
+            if (s_dead[s]) continue;
+            const SlotDev& sl = P.slot[s];
+            const int j = s_j[s];
+            C* stg = P.sense == PTY_SENSE_XCORR_B ? reinterpret_cast<C*>(sl.stage) + (size_t)j * 2 * WW : nullptr;
+            task_col_mod<T, W>(tw, xch, b, gmask, scratch + (size_t)s * M * WW, M, kc, totT + (size_t)s * WW,
+                               tmax_part + (size_t)s * W, reinterpret_cast<const T*>(sl.patterns_t) + (size_t)j * WW,
+                               T(P.eps_rel), P.track_mod, stg,
+                               P.err_part + (((size_t)s * N + step) * W + kc) * 3);
+        }
         stamp(step, 3);
         bar.sync();
-        X.phase4(step);
+        // --------------------------------------- P4 rows (inverse) + update
+        for (int task = blockIdx.x * NTEAM + team; task < S * nq; task += gridDim.x * NTEAM) {
+            const int s = task / nq, rq = task % nq;
+            if (s_dead[s]) continue;
+            const SlotDev& sl = P.slot[s];
+            const int j = s_j[s];
+            const T* pkp = peak_part + ((size_t)(step & 1) * S + s) * nq;
+            const T* omp = omax_part + (size_t)s * nq;
+            T peak = T(0), omax = T(0);
+            for (int q = b; q < nq; q += B) {
+                peak = fmax(peak, pkp[q]);
+                omax = fmax(omax, omp[q]);
+            }
+            peak = group_max<B>(peak);
+            omax = group_max<B>(omax);
+            if (peak == T(0)) {                                // engine.py:132-134
+                if (tl == 0) atomicOr(sl.status, PTY_ERR_PROBE_ZERO);
+                continue;
+            }
+            if (P.update_probe && omax == T(0)) {              // engine.py:145-147
+                if (tl == 0) atomicOr(sl.status, PTY_ERR_OBJECT_ZERO);
+                continue;
+            }
+            C* stg = P.sense == PTY_SENSE_XCORR_A ? reinterpret_cast<C*>(sl.stage) + (size_t)j * 2 * WW : nullptr;
+            const T npk = task_row_inv_update<T, W>(tw, lines, numer, ppacc, nppacc, red4_p4, team, tl, gi, b, gmask,
+                                                    scratch + (size_t)s * M * WW, M, rq, reinterpret_cast<C*>(sl.obj),
+                                                    sl.Wc, s_ar[s], s_ac[s], reinterpret_cast<C*>(sl.probes), peak,
+                                                    omax, U, stg);
+            if (tl == 0) peak_part[((size_t)((step + 1) & 1) * S + s) * nq + rq] = npk;
+        }
         stamp(step, 4);
         bar.sync();
     }
 }
 
 // Deterministic end-of-sweep reduction of the per-visit error partials
-// (engine.py:198-202, 239-241): one CTA per slot, thread t sums visits
-// t, t+256, ... in order, then a fixed shuffle tree -- same order every run.
+// (engine.py:198-202, 239-241) in two fixed-order levels: one CTA per visit
+// reduces its nCT column partials, then one CTA per slot reduces the visits.
 struct ErrOut {
     double* p[kMaxSlots];
 };
-static __global__ void __launch_bounds__(256) sweep_finalize_kernel(const double* err_part, int N, int nCT,
-                                                                    int nslots, ErrOut outs) {
+static __global__ void __launch_bounds__(256) err_visit_kernel(const double* err_part, int nCT, double* visit_sum) {
+    __shared__ double red[32];
+    const size_t v = blockIdx.x;
+    double num = 0.0, den = 0.0, worst = 0.0;
+    for (int ct = threadIdx.x; ct < nCT; ct += blockDim.x) {
+        const double* e = err_part + (v * nCT + ct) * 3;
+        num += e[0];
+        den += e[1];
+        worst = fmax(worst, e[2]);
+    }
+    num = block_sum(num, red);
+    den = block_sum(den, red);
+    worst = block_max(worst, red);
+    if (threadIdx.x == 0) {
+        visit_sum[v * 3] = num;
+        visit_sum[v * 3 + 1] = den;
+        visit_sum[v * 3 + 2] = worst;
+    }
+}
+static __global__ void __launch_bounds__(256) err_slot_kernel(const double* visit_sum, int N, int nslots, ErrOut outs) {
     __shared__ double red[32];
     const int s = blockIdx.x;
     if (s >= nslots) return;
     double num = 0.0, den = 0.0, worst = 0.0;
     for (int k = threadIdx.x; k < N; k += blockDim.x) {
-        for (int ct = 0; ct < nCT; ++ct) {
-            const double* e = err_part + (((size_t)s * N + k) * nCT + ct) * 3;
-            num += e[0];
-            den += e[1];
-            worst = fmax(worst, e[2]);
-        }
+        const double* e = visit_sum + ((size_t)s * N + k) * 3;
+        num += e[0];
+        den += e[1];
+        worst = fmax(worst, e[2]);
     }
     num = block_sum(num, red);
     den = block_sum(den, red);

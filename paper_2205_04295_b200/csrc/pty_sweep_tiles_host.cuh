@@ -1,25 +1,25 @@
-// pty_sweep_host.cuh -- host side of pty_sweep: workspace layout, tile-size
+// pty_sweep_tiles_host.cuh -- host side of the latency variant of pty_sweep: workspace layout, tile-size
 // choice and the cooperative launch of sweep_kernel<T, W>.  Explicitly
 // instantiated per (dtype, window) in pty_sweep_*.cu so the kernels compile in
 // parallel translation units.
 #pragma once
 #include "pty_host.cuh"
-#include "pty_sweep.cuh"
-#include "pty_sweep_tiles_host.cuh"
+#include "pty_sweep_tiles.cuh"
 
 namespace pty {
+namespace tiles {
 
 // ------------------------------------------------------------- sweep ------
+constexpr int kMinTC = 4;   // column tiles are >= 4 complex (32-byte sectors)
+
 struct SweepLayout {
     unsigned int* barrier;
     int* anchors;
     void* scratch;
-    void* totT;
     void* omax;
     void* peak;
     void* tmax;
     double* err_part;
-    double* visit_sum;
     size_t bytes;
 };
 
@@ -30,35 +30,16 @@ inline SweepLayout carve_sweep(void* ws, int W, int M, int N, int S) {
     L.barrier = c.take<unsigned int>(sizeof(unsigned int));
     L.anchors = c.take<int>((size_t)S * N * 2 * sizeof(int));
     L.scratch = c.take<void>((size_t)S * M * W * W * sizeof(cplx<T>));
-    L.totT = c.take<void>((size_t)S * W * W * sizeof(T));
-    L.omax = c.take<void>((size_t)S * (W / 4) * sizeof(T));
-    L.peak = c.take<void>((size_t)2 * S * (W / 4) * sizeof(T));
+    L.omax = c.take<void>((size_t)S * W * sizeof(T));
+    L.peak = c.take<void>((size_t)2 * S * W * sizeof(T));
     L.tmax = c.take<void>((size_t)S * W * sizeof(T));
-    L.err_part = c.take<double>((size_t)S * N * W * 3 * sizeof(double));
-    L.visit_sum = c.take<double>((size_t)S * N * 3 * sizeof(double));
+    L.err_part = c.take<double>((size_t)S * N * (W / kMinTC) * 3 * sizeof(double));
     L.bytes = c.off;
     return L;
 }
 
-// few slots (latency): the tile kernel; many slots (throughput): line tasks.
-inline int tiles_max_slots() { return env_int("PTY_SWEEP_TILES_MAX", 8); }
-
-template <typename T>
-inline size_t sweep_workspace(int W, int M, int N, int S) {
-    return std::max(carve_sweep<T>(nullptr, W, M, N, S).bytes, tiles::carve_sweep<T>(nullptr, W, M, N, S).bytes);
-}
-
-template <typename T, int W>
-int run_sweep_lines(const PtySweepArgs* a, cudaStream_t st);
-
 template <typename T, int W>
 int run_sweep(const PtySweepArgs* a, cudaStream_t st) {
-    if (a->n_slots <= tiles_max_slots()) return tiles::run_sweep<T, W>(a, st);
-    return run_sweep_lines<T, W>(a, st);
-}
-
-template <typename T, int W>
-int run_sweep_lines(const PtySweepArgs* a, cudaStream_t st) {
     const int M = a->modes, N = a->n_positions, S = a->n_slots;
     SweepLayout L = carve_sweep<T>(a->workspace, W, M, N, S);
     if (!a->workspace || a->workspace_bytes < (int64_t)L.bytes) return PTY_ERR_ARGUMENT;
@@ -70,35 +51,61 @@ int run_sweep_lines(const PtySweepArgs* a, cudaStream_t st) {
     P.alpha_o = a->alpha_obj; P.alpha_p = a->alpha_probe; P.beta = a->beta; P.gamma = a->gamma;
     P.eps_rel = a->epsilon_rel;
     P.update_probe = a->update_probe; P.track_mod = a->track_modulus; P.sense = a->sense;
-    P.barrier = L.barrier; P.anchors = L.anchors; P.scratch = L.scratch; P.totT = L.totT;
+    P.barrier = L.barrier; P.anchors = L.anchors; P.scratch = L.scratch;
     P.omax_part = L.omax; P.peak_part = L.peak; P.tmax_part = L.tmax;
     P.err_part = L.err_part; P.twiddles = tw;
     ErrOut outs{};
     for (int s = 0; s < S; ++s) {
         const PtySlot& h = a->slots[s];
-        if (!h.obj || !h.probes || !h.patterns || !h.patterns_t || !h.positions || !h.order || !h.status || !h.err_out)
+        if (!h.obj || !h.probes || !h.patterns || !h.positions || !h.order || !h.status || !h.err_out)
             return PTY_ERR_ARGUMENT;
         if (a->sense != PTY_SENSE_NONE && !h.stage) return PTY_ERR_ARGUMENT;
         if (h.H < W || h.Wc < W) return PTY_ERR_ARGUMENT;
-        P.slot[s] = SlotDev{h.obj, h.H, h.Wc, h.r0, h.c0, h.probes, h.patterns, h.patterns_t, h.positions,
+        P.slot[s] = SlotDev{h.obj, h.H, h.Wc, h.r0, h.c0, h.probes, h.patterns, h.positions,
                             h.order, h.stage, h.err_out, h.status};
         outs.p[s] = h.err_out;
     }
 
-    // launch geometry: kSweepThreads-thread CTAs, as many per SM as fit (<= 2),
-    // cooperative (all co-resident); PTY_CTAS_PER_SM overrides downwards.
-    const size_t smem = sweep_smem_fixed<T, W>() + sweep_smem_phase<T, W>(kSweepThreads);
+    // launch geometry: kSweepThreads-thread CTAs, `per_sm` of them per SM
+    // (default 2 so one CTA's loads overlap the other's FFTs), cooperative.
+    // Tiles: the smallest power-of-two rows/columns per item that keep the
+    // item count <= the CTA count (every CTA busy even for one reconstruction),
+    // bounded by the per-CTA shared-memory budget.  PTY_TR / PTY_TC /
+    // PTY_CTAS_PER_SM override (tuning).
+    const int sms = sm_count();
+    int per_sm = std::max(1, env_int("PTY_CTAS_PER_SM", kSweepMinCtasPerSm));
+    const size_t smem_sm = max_smem_per_sm();
+    const size_t fixed = sweep_smem_fixed<T, W>();
+    const size_t budget = std::min(max_dyn_smem(), smem_sm / per_sm - 1024 - 512) - fixed;
+    const int grid = sms * per_sm;
+    constexpr int LS = line_stride<W>();
+    const size_t line_bytes = (size_t)LS * sizeof(cplx<T>);
+    int TR = env_int("PTY_TR", 0);
+    if (TR <= 0) {
+        TR = 1;
+        while (TR < W && (long)S * (W / TR) > grid && (size_t)2 * TR * M * line_bytes <= budget) TR *= 2;
+    }
+    int TC = env_int("PTY_TC", 0);
+    if (TC <= 0) {
+        TC = kMinTC;
+        while (TC < W && (long)S * (W / TC) > grid && (size_t)2 * TC * M * line_bytes <= budget) TC *= 2;
+    }
+    if (TR < 1 || TR > W || (W % TR) || TC < kMinTC || TC > W || (W % TC)) return PTY_ERR_ARGUMENT;
+    const int nRT = W / TR, nCT = W / TC;
+    const int K = (S * nCT + grid - 1) / grid;
+    const size_t tile_bytes = std::max((size_t)TR * M * line_bytes, (size_t)K * M * TC * line_bytes);
+    if (tile_bytes > budget) return PTY_ERR_ARGUMENT;   // too many replicas for the resident column tiles
+    P.TR = TR; P.TC = TC; P.nRT = nRT; P.nCT = nCT; P.K = K;
+    P.lgTR = 0; while ((1 << P.lgTR) < TR) ++P.lgTR;
+    P.lgTC = 0; while ((1 << P.lgTC) < TC) ++P.lgTC;
+    const size_t smem = fixed + tile_bytes;
+
     auto kern = sweep_kernel<T, W>;
-    if (smem > max_dyn_smem()) return PTY_ERR_ARGUMENT;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return PTY_ERR_CUDA;
     int fit = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, kern, kSweepThreads, smem) != cudaSuccess || fit < 1)
-        return PTY_ERR_CUDA;
-    int per_sm = std::min(fit, kSweepMaxCtasPerSm);
-    const int want = env_int("PTY_CTAS_PER_SM", 0);
-    if (want > 0) per_sm = std::min(per_sm, want);
-    const int grid = sm_count() * per_sm;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, kern, kSweepThreads, smem) != cudaSuccess || fit < per_sm)
+        return PTY_ERR_CUDA;   // the cooperative grid must be co-resident
 
     // debug timeline (PTY_TIMELINE=<steps>): per-CTA phase completion stamps
     const int tl_steps = std::min(env_int("PTY_TIMELINE", 0), N);
@@ -109,14 +116,13 @@ int run_sweep_lines(const PtySweepArgs* a, cudaStream_t st) {
         P.timeline_steps = tl_steps;
     }
     if (cudaMemsetAsync(L.barrier, 0, sizeof(unsigned int), st) != cudaSuccess) return PTY_ERR_CUDA;
-    if (cudaMemsetAsync(L.err_part, 0, (size_t)S * N * W * 3 * sizeof(double), st) != cudaSuccess)
+    if (cudaMemsetAsync(L.err_part, 0, (size_t)S * N * nCT * 3 * sizeof(double), st) != cudaSuccess)
         return PTY_ERR_CUDA;
     void* args[] = {&P};
     cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kSweepThreads), args, smem, st);
     if (e != cudaSuccess) return PTY_ERR_CUDA;
-    err_visit_kernel<<<S * N, 256, 0, st>>>(L.err_part, W, L.visit_sum);
-    err_slot_kernel<<<S, 256, 0, st>>>(L.visit_sum, N, S, outs);
-    count(3);
+    sweep_finalize_kernel<<<S, 256, 0, st>>>(L.err_part, N, nCT, S, outs);
+    count(2);
     if (tl) {
         g_timeline.assign((size_t)tl_steps * 5 * grid, 0ull);
         cudaMemcpyAsync(g_timeline.data(), tl, g_timeline.size() * sizeof(unsigned long long),
@@ -128,4 +134,6 @@ int run_sweep_lines(const PtySweepArgs* a, cudaStream_t st) {
     return last_status();
 }
 
+
+}  // namespace tiles
 }  // namespace pty

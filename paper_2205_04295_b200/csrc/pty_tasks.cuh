@@ -1,0 +1,299 @@
+// pty_tasks.cuh -- the per-line task bodies shared by the reference-order
+// sweep kernel (pty_sweep.cuh) and the batched kernels (pty_batched.cuh).
+//
+// Vocabulary: a "group" is B threads that transform one W-line with the
+// fused-I/O group_fft (stage-1 loads straight from global memory, stage-2
+// outputs straight into the epilogue); a "team" is 4 groups owning 4
+// consecutive rows, so transposed accesses move 4 consecutive complex values
+// (one 32-byte sector) per column.  Scratch layout per position:
+//   [m][kc][r]  after the row pass (row-DFT output transposed), so the column
+//   passes read and write contiguous lines; totT[kc][u] = total detector
+//   intensity transposed.
+#pragma once
+#include "pty_fft.cuh"
+
+namespace pty {
+
+template <int TEAM>
+__device__ __forceinline__ void team_sync(int team) {
+    if constexpr (TEAM <= 32) {
+        const unsigned lane = threadIdx.x & 31;
+        const unsigned m = TEAM == 32 ? 0xffffffffu : (((1u << TEAM) - 1u) << (lane & ~(unsigned)(TEAM - 1)));
+        __syncwarp(m);
+    } else {
+        asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "r"(TEAM) : "memory");
+    }
+}
+
+// max / sum over the B lanes of a group (B divides 32)
+template <int B, typename T>
+__device__ __forceinline__ T group_max(T v) {
+#pragma unroll
+    for (int o = B / 2; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+template <int B, typename T>
+__device__ __forceinline__ T group_sum(T v) {
+#pragma unroll
+    for (int o = B / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <int W> __device__ __forceinline__ unsigned group_mask() {
+    constexpr int B = Shape<W>::B;
+    const unsigned lane = threadIdx.x & 31;
+    return B == 32 ? 0xffffffffu : (((1u << B) - 1u) << (lane & ~(unsigned)(B - 1)));
+}
+
+// line stride of the team lines: >= W + W/B + 1 and = 4 (mod 16) so that the
+// 4-row transposed stores hit distinct banks
+template <int W> __host__ __device__ constexpr int team_line_stride() {
+    return ((W + W / Shape<W>::B + 1 + 11) / 16) * 16 + 4;
+}
+
+// output column of stage-2 slot q for group lane b
+template <int W> __device__ __forceinline__ int slot_col(int b, int q) {
+    constexpr int A = Shape<W>::A, B = Shape<W>::B;
+    return b + B * (q / B) + A * (q % B);
+}
+
+// Team-level max of one value per group (4 groups); red4 = 4 shared slots of the team.
+template <int W, typename T>
+__device__ __forceinline__ T team_max4(T v, T* red4, int team, int gi, int b) {
+    constexpr int B = Shape<W>::B, TEAM = 4 * B;
+    v = group_max<B>(v);
+    if (b == 0) red4[gi] = v;
+    team_sync<TEAM>(team);
+    const T r = fmax(fmax(red4[0], red4[1]), fmax(red4[2], red4[3]));
+    team_sync<TEAM>(team);
+    return r;
+}
+
+// Row pass, team task (mode m, row quad rq) of one position (engine.py:113,
+// fields.py:81): exit waves C * P_m * o_j, row DFTs, output transposed into
+// dst = the position's scratch.  Returns the team's max|o|^2 when m == 0
+// (engine.py:145); stg_o (row-major o_j, XCORR_A sensor input) may be null.
+template <typename T, int W>
+__device__ __forceinline__ T task_row_fwd(const cplx<T>* tw, cplx<T>* xch, cplx<T>* tt, T* red4, int team, int tl,
+                                          int gi, int b, unsigned gmask, const cplx<T>* obj, int Wc, int ar, int ac,
+                                          const cplx<T>* probes, int m, int rq, cplx<T>* dst_pos, cplx<T>* stg_o) {
+    using C = cplx<T>;
+    constexpr int B = Shape<W>::B, TEAM = 4 * B;
+    const size_t WW = (size_t)W * W;
+    const int r = 4 * rq + gi;
+    const C* orow = obj + (size_t)(ar + r) * Wc + ac;
+    const C* prow = probes + m * WW + (size_t)r * W;
+    C* stg = stg_o ? stg_o + (size_t)r * W : nullptr;
+    T om = T(0);
+    group_fft<T, W, false>(
+        xch, tw, b, gmask,
+        [&](int n, int) {
+            const C o = orow[n];
+            if (m == 0) {
+                om = fmax(om, norm2(o));
+                if (stg) stg[n] = o;
+            }
+            return scale(prow[n] * o, checker<T>(r, n));
+        },
+        [&](int kc, int, C v) { tt[kc * 5 + gi] = v; });
+    team_sync<TEAM>(team);
+    C* dst = dst_pos + m * WW + 4 * rq;
+    for (int e = tl; e < 4 * W; e += TEAM) dst[(size_t)(e >> 2) * W + (e & 3)] = tt[(e >> 2) * 5 + (e & 3)];
+    T res = T(0);
+    if (m == 0) res = team_max4<W>(om, red4, team, gi, b);
+    team_sync<TEAM>(team);
+    return res;
+}
+
+// Column pass, group task (column kc) of one position: forward column DFTs of
+// every mode written back in place (Psi), total = sum_m |Psi_m|^2 (engine.py:
+// 114-116) stored transposed; returns the column's max(total).
+template <typename T, int W>
+__device__ __forceinline__ T task_col_fwd(const cplx<T>* tw, cplx<T>* xch, int b, unsigned gmask, cplx<T>* pos, int M,
+                                          int kc, T* totT_pos) {
+    using C = cplx<T>;
+    constexpr int A = Shape<W>::A, B = Shape<W>::B;
+    const size_t WW = (size_t)W * W;
+    const T invW2 = T(1) / (T(W) * T(W));
+    T tot[A];
+#pragma unroll
+    for (int q = 0; q < A; ++q) tot[q] = T(0);
+    for (int m = 0; m < M; ++m) {
+        C* line = pos + m * WW + (size_t)kc * W;
+        group_fft<T, W, false>(
+            xch, tw, b, gmask, [&](int n, int) { return line[n]; },
+            [&](int u, int slot, C v) {
+                line[u] = v;
+                tot[slot] += norm2(v) * invW2;
+            });
+    }
+    T tm = T(0);
+    T* trow = totT_pos + (size_t)kc * W;
+#pragma unroll
+    for (int q = 0; q < A; ++q) {
+        trow[slot_col<W>(b, q)] = tot[q];
+        tm = fmax(tm, tot[q]);
+    }
+    return group_max<B>(tm);
+}
+
+// Column pass 2, group task (column kc): modulus constraint
+// scale = sqrt(I)/sqrt(total + eps) (engine.py:117-118), error terms
+// (engine.py:198-214) and inverse column DFTs of every mode.
+// tmax_pos: the position's W column maxima; It: the transposed pattern.
+// stg (XCORR_B sensor planes, row-major total and I) may be null.
+// Writes err[0..2] = (sum (sqrt(total)-sqrt(I))^2, sum I, worst modulus error).
+template <typename T, int W>
+__device__ __forceinline__ void task_col_mod(const cplx<T>* tw, cplx<T>* xch, int b, unsigned gmask, cplx<T>* pos,
+                                             int M, int kc, const T* totT_pos, const T* tmax_pos, const T* It_pos,
+                                             T eps_rel, int track, cplx<T>* stg, double* err) {
+    using C = cplx<T>;
+    constexpr int A = Shape<W>::A, B = Shape<W>::B;
+    const size_t WW = (size_t)W * W;
+    const T invW2 = T(1) / (T(W) * T(W));
+    T tmax = T(0);
+    for (int q = b; q < W; q += B) tmax = fmax(tmax, tmax_pos[q]);
+    tmax = group_max<B>(tmax);
+    const T eps = eps_rel * fmax(tmax, real_limits<T>::tiny());
+    const T* It = It_pos + (size_t)kc * W;
+    const T* tt = totT_pos + (size_t)kc * W;
+    T sc[A], after[A];
+    double en = 0.0, ed = 0.0;
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+        const int u = B * a + b;
+        const T Iv = It[u], tv = tt[u];
+        const T sI = sqrt_rn(Iv);
+        sc[a] = sI / sqrt_rn(tv + eps);
+        const T d = sqrt_rn(tv) - sI;
+        en += (double)(d * d);
+        ed += (double)Iv;
+        after[a] = T(0);
+        if (stg) {
+            stg[(size_t)u * W + kc] = C{tv, T(0)};
+            stg[WW + (size_t)u * W + kc] = C{Iv, T(0)};
+        }
+    }
+    for (int m = 0; m < M; ++m) {
+        C* line = pos + m * WW + (size_t)kc * W;
+        group_fft<T, W, true>(
+            xch, tw, b, gmask,
+            [&](int n, int a) {
+                const C v = scale(line[n], sc[a]);
+                after[a] += norm2(v) * invW2;
+                return v;
+            },
+            [&](int r, int, C v) { line[r] = v; });
+    }
+    T worst = T(0);
+    if (track) {
+#pragma unroll
+        for (int a = 0; a < A; ++a) {
+            const int u = B * a + b;
+            const T Iv = It[u], tv = tt[u];
+            if (tv > T(1e-3) * tmax) worst = fmax(worst, fabs(after[a] - Iv) / fmax(Iv, real_limits<T>::tiny()));
+        }
+    }
+    en = group_sum<B>(en);
+    ed = group_sum<B>(ed);
+    worst = group_max<B>(worst);
+    if (b == 0) {
+        err[0] = en;
+        err[1] = ed;
+        err[2] = (double)worst;
+    }
+}
+
+// Team load of one mode's 4 rows from the transposed scratch into the team's
+// padded lines (natural order along kc).
+template <typename T, int W>
+__device__ __forceinline__ void team_load_rows(cplx<T>* lines, const cplx<T>* src_mode, int rq, int tl) {
+    constexpr int B = Shape<W>::B, TEAM = 4 * B, LS4 = team_line_stride<W>();
+    const cplx<T>* src = src_mode + 4 * rq;
+    for (int e = tl; e < 4 * W; e += TEAM) lines[(e & 3) * LS4 + pad<W>(e >> 2)] = src[(size_t)(e >> 2) * W + (e & 3)];
+}
+
+struct UpdateParams {
+    double alpha_o, alpha_p, beta, gamma, eps_rel;
+    int update_probe;
+};
+
+// Row pass 2 of the reference-order sweep, team task (row quad rq) of one
+// position: inverse row DFTs of every mode -> corrected exit waves psi'
+// (engine.py:119); object update with the paste-add rounding (engine.py:123-137,
+// fields.py:101-107) and in-place probe update with the pre-update o_j and
+// probes (engine.py:140-150, 218-223).  numer/pp/nppacc: the team's [4][W]
+// shared accumulators (owner-only access).  Returns the team's max of the next
+// visit's sum_m |P_m|^2 (engine.py:129-132).  stg (XCORR_A planes) may be null.
+template <typename T, int W>
+__device__ __forceinline__ T task_row_inv_update(const cplx<T>* tw, cplx<T>* lines, cplx<T>* numer, T* pp, T* nppacc,
+                                                 T* red4,
+                                                 int team, int tl, int gi, int b, unsigned gmask, const cplx<T>* pos,
+                                                 int M, int rq, cplx<T>* obj, int Wc, int ar, int ac, cplx<T>* probes,
+                                                 T peak, T omax, const UpdateParams& U, cplx<T>* stg) {
+    using C = cplx<T>;
+    constexpr int A = Shape<W>::A, B = Shape<W>::B, TEAM = 4 * B, LS4 = team_line_stride<W>();
+    const size_t WW = (size_t)W * W;
+    const T invW2 = T(1) / (T(W) * T(W));
+    const T alpha_o = T(U.alpha_o), alpha_p = T(U.alpha_p), beta = T(U.beta), gamma = T(U.gamma),
+            eps_rel = T(U.eps_rel);
+    const int r = 4 * rq + gi;
+    C* orow = obj + (size_t)(ar + r) * Wc + ac;
+    C* myline = lines + gi * LS4;
+    C* nrow = numer + gi * W;
+    T* prow_pp = pp + gi * W;
+    T* npp = nppacc + gi * W;
+    C ov[A];
+#pragma unroll
+    for (int q = 0; q < A; ++q) {
+        const int c = slot_col<W>(b, q);
+        ov[q] = orow[c];
+        nrow[c] = C{T(0), T(0)};
+        prow_pp[c] = T(0);
+        npp[c] = T(0);
+    }
+    const T dmax_p = beta * omax + (T(1) - beta) * omax;
+    for (int m = 0; m < M; ++m) {
+        team_sync<TEAM>(team);
+        team_load_rows<T, W>(lines, pos + m * WW, rq, tl);
+        C* pr = probes + m * WW + (size_t)r * W;
+        C pv[A];
+#pragma unroll
+        for (int q = 0; q < A; ++q) pv[q] = pr[slot_col<W>(b, q)];
+        team_sync<TEAM>(team);
+        group_fft<T, W, true>(
+            myline, tw, b, gmask, [&](int n, int) { return myline[pad<W>(n)]; },
+            [&](int c, int q, C X) {
+                const C o = ov[q];
+                const C d = scale(X, checker<T>(r, c) * invW2) - pv[q] * o;
+                nrow[c] = nrow[c] + mulc(d, pv[q]);
+                prow_pp[c] += norm2(pv[q]);
+                if (U.update_probe) {
+                    T dp = beta * omax + (T(1) - beta) * norm2(o);
+                    dp = dp + eps_rel * dmax_p;
+                    const C np_ = pv[q] + divr(mulc(scale(d, alpha_p), o), dp);
+                    pr[c] = np_;
+                    npp[c] += norm2(np_);
+                }
+            });
+    }
+    const T dmax_o = gamma * peak + (T(1) - gamma) * peak;
+    T pk = T(0);
+#pragma unroll
+    for (int q = 0; q < A; ++q) {
+        const int c = slot_col<W>(b, q);
+        const C o = ov[q];
+        T den = gamma * peak + (T(1) - gamma) * prow_pp[c];
+        den = den + eps_rel * dmax_o;
+        const C no = o + divr(scale(nrow[c], alpha_o), den);
+        orow[c] = o + (no - o);                                // paste_add_inplace
+        if (stg) {
+            stg[(size_t)r * W + c] = o;
+            stg[WW + (size_t)r * W + c] = no;
+        }
+        pk = fmax(pk, U.update_probe ? npp[c] : prow_pp[c]);
+    }
+    return team_max4<W>(pk, red4, team, gi, b);
+}
+
+}  // namespace pty

@@ -147,19 +147,36 @@ def _dtypes(precision: str):
     return (t.complex64, t.float32) if precision == "fp32" else (t.complex128, t.float64)
 
 
-_PATTERN_CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_SHADOWS: dict = {}
+
+
+def _shadow(dataset):
+    """Our PtychoDataset for a foreign dataset object (e.g. ptychokit's): it
+    carries the cached device copies; dropped when the original dies."""
+    from .dataio import PtychoDataset
+    if isinstance(dataset, PtychoDataset):
+        return dataset
+    key = id(dataset)
+    ent = _SHADOWS.get(key)
+    if ent is None or ent[0]() is not dataset or ent[1].patterns is not dataset.patterns:
+        shadow = PtychoDataset(dataset.patterns, dataset.positions, dataset.geometry)
+        try:
+            ref = weakref.ref(dataset, lambda _r, k=key: _SHADOWS.pop(k, None))
+        except TypeError:
+            ref = (lambda d=dataset: d)
+        _SHADOWS[key] = (ref, shadow)
+        ent = _SHADOWS[key]
+    return ent[1]
 
 
 def device_patterns(dataset, real_dtype):
     """The dataset's diffraction stack in HBM (uploaded once, I >= 0 checked)."""
-    if hasattr(dataset, "device_patterns"):
-        return dataset.device_patterns(real_dtype)
-    from .dataio import PtychoDataset
-    shadow = _PATTERN_CACHE.get(dataset)
-    if shadow is None or shadow.patterns is not dataset.patterns:
-        shadow = PtychoDataset(dataset.patterns, dataset.positions, dataset.geometry)
-        _PATTERN_CACHE[dataset] = shadow
-    return shadow.device_patterns(real_dtype)
+    return _shadow(dataset).device_patterns(real_dtype)
+
+
+def device_patterns_t(dataset, real_dtype):
+    """Per-pattern transposed copy I^T[j][kc][u] (the column passes' layout)."""
+    return _shadow(dataset).device_patterns_t(real_dtype)
 
 
 def initialize(dataset, config: SolverConfig) -> ReconState:
@@ -253,6 +270,7 @@ def sweep_batched(state: ReconState, dataset, config: SolverConfig, group=None) 
     if engaged:
         sense = _native.SENSE_XCORR_A if config.posref.sensor == "XCORR_A" else _native.SENSE_XCORR_B
     pats = device_patterns(ds, rdt)
+    pats_t = device_patterns_t(ds, rdt)
     order = visit_order(n, config, st.iteration)
     b = min(config.batch_size, n)
     h, wc = st.obj.shape
@@ -261,7 +279,7 @@ def sweep_batched(state: ReconState, dataset, config: SolverConfig, group=None) 
     status = st.buffer("status", (1,), t.int32)
     status.zero_()
     err = st.buffer("err", (3,), t.float64)
-    err_part = st.buffer("err_part", (n, w // 4, 3), t.float64)
+    err_part = st.buffer("err_part", (n, w, 3), t.float64)
     err_part.zero_()
     obj_acc = st.buffer("obj_acc", (3, h, wc), rdt)
     probe_acc = st.buffer("probe_acc", (2 * m + 1, w, w), rdt)
@@ -278,7 +296,7 @@ def sweep_batched(state: ReconState, dataset, config: SolverConfig, group=None) 
         if hi > lo:
             args = _native.PtyBatchArgs(
                 dcode, w, m, n, _native.ptr(st.obj), h, wc, st.canvas_origin[0], st.canvas_origin[1],
-                _native.ptr(st.probe_stack), _native.ptr(pats), _native.ptr(st.positions),
+                _native.ptr(st.probe_stack), _native.ptr(pats), _native.ptr(pats_t), _native.ptr(st.positions),
                 _native.ptr(order_d) + 4 * (s + lo), hi - lo, s + lo,
                 float(config.alpha_obj), float(config.alpha_probe), float(config.beta),
                 float(config.gamma), float(config.epsilon_rel), upd_probe,
@@ -295,7 +313,7 @@ def sweep_batched(state: ReconState, dataset, config: SolverConfig, group=None) 
             dist.all_reduce(probe_acc, group=group)
         args = _native.PtyBatchArgs(
             dcode, w, m, n, _native.ptr(st.obj), h, wc, st.canvas_origin[0], st.canvas_origin[1],
-            _native.ptr(st.probe_stack), _native.ptr(pats), _native.ptr(st.positions),
+            _native.ptr(st.probe_stack), _native.ptr(pats), _native.ptr(pats_t), _native.ptr(st.positions),
             _native.ptr(order_d) + 4 * (s + lo), max(hi - lo, 1), s + min(lo, nb - 1),
             float(config.alpha_obj), float(config.alpha_probe), float(config.beta),
             float(config.gamma), float(config.epsilon_rel), upd_probe,
@@ -358,6 +376,7 @@ def sweep_replicas(states, datasets, config: SolverConfig, orders=None, kernel_e
                 or st.probe_stack.shape[0] != m:
             raise ShapeError("replicas must share window, mode count, positions and precision")
         pats = device_patterns(ds, rdt)
+        pats_t = device_patterns_t(ds, rdt)
         order = orders[k] if orders is not None else visit_order(n, config, st.iteration)
         order_h = st.buffer("order", (n,), t.int32, pinned=True)
         order_h.numpy()[:] = order
@@ -371,10 +390,10 @@ def sweep_replicas(states, datasets, config: SolverConfig, orders=None, kernel_e
         st.probe_stack = st.probe_stack.contiguous()
         h, wc = st.obj.shape
         slots[k] = _native.PtySlot(_native.ptr(st.obj), h, wc, st.canvas_origin[0], st.canvas_origin[1],
-                                   _native.ptr(st.probe_stack), _native.ptr(pats),
+                                   _native.ptr(st.probe_stack), _native.ptr(pats), _native.ptr(pats_t),
                                    _native.ptr(st.positions), _native.ptr(order_d),
                                    _native.ptr(stage), _native.ptr(err), _native.ptr(status))
-        keep.append((pats, order_d))
+        keep.append((pats, pats_t, order_d))
     nbytes = _native.sweep_workspace_bytes(dcode, w, m, n, len(states))
     ws = _native.workspace(nbytes)
     args = _native.PtySweepArgs(

