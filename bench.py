@@ -265,6 +265,53 @@ def e2e_arm(args, states, ds, cfg, dev, world):
             "d2h_bytes_per_step": int(d2h)}
 
 
+# ----------------------------------------------- batched leg (config 5) ----
+def batched_leg(args, rank, world):
+    """BASELINE configs[4]: batched semi-parallel rPIE, 6400 positions of
+    256x256x3; every batch is split across the ranks and the update terms are
+    all-reduced (NCCL) once per batch (strong scaling over ranks)."""
+    import torch
+    import paper_2205_04295_b200 as pk
+    global GRID
+    grid0 = GRID
+    GRID = (80, 80)
+    try:
+        ds = make_dataset(seed=5)
+    finally:
+        GRID = grid0
+    n = ds.n_positions
+    b = args.batch
+    cfg = pk.SolverConfig(**{**solver_config(args.precision).__dict__, "batch_size": b})
+    group = torch.distributed.group.WORLD if world > 1 else None
+    st = pk.initialize(ds, cfg)
+    for _ in range(2):
+        pk.sweep(st, ds, cfg, group=group)
+    ms = []
+    for _ in range(max(2, args.steps // 2)):
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        pk.sweep(st, ds, cfg, group=group)
+        e.record()
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(e))
+    total = sum(ms)
+    if world > 1:
+        t = torch.tensor([total], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total = t.item()
+    per = total / len(ms)
+    hbm, _ = peaks()
+    value = n / (per / 1e3)
+    return {"workload": "config 5: batched semi-parallel rPIE, 80x80 scan (6400 positions), 256x256x3 modes, "
+                        f"batch {b} split over {world} GPU(s), NCCL all-reduce of the update terms per batch",
+            "value": value, "unit": "positions/s", "ms_per_iteration": per, "iterations_per_s": 1e3 / per,
+            "scaling": "strong", "roofline_frac": value * B_POS / (hbm * 1e9 * world),
+            "error_trace_last": st.error_trace[-1]}
+
+
 # ------------------------------------------------------- CPU reference ----
 def _cpu_worker(payload):
     os.environ.setdefault("OMP_NUM_THREADS", "1")
@@ -369,6 +416,8 @@ def main():
     ap.add_argument("--cpu-workers", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-single", action="store_true")
+    ap.add_argument("--no-batched", action="store_true")
+    ap.add_argument("--batch", type=int, default=1600)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
 
@@ -404,6 +453,12 @@ def main():
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         torch.distributed.init_process_group("nccl")
     res = gpu_arm(args, rank, world)
+    batched = None
+    if not args.no_batched:
+        try:
+            batched = batched_leg(args, rank, world)
+        except Exception as exc:                      # report, never lose the main line
+            batched = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         vals = cpu_reference(workers, args.cpu_sample, 1)
@@ -431,6 +486,7 @@ def main():
             "gpu_launches": res["launches"],
             "clocks": res["clocks"],
             "single_reconstruction": res["single"],
+            "batched": batched,
             "iterations_per_s": 1e3 / res["ms_per_step"],
         }
         print(json.dumps(line), flush=True)

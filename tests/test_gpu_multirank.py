@@ -1,0 +1,68 @@
+"""The engine's multi-rank batched sweep (sweep_batched with a process group)
+on ONE GPU: two processes share the device, each runs its share of every batch
+through the CUDA kernels and the update terms are all-reduced with gloo (host
+copies; no kernel waits on another).  Result == the single-process batched
+sweep of the same batches (the NCCL path on 2-8 GPUs runs the same code)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _run(rank, world, port, q):
+    import torch.distributed as dist
+    import paper_2205_04295_b200 as pk
+    from test_gpu_parity import make_ds, pkg_cfg
+    from test_oracle_golden import cfg_from_repr
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    g = golden("sweep_rpie")
+    c = pkg_cfg(cfg_from_repr(str(g["cfg_repr"])), "fp64")
+    cfg = pk.SolverConfig(**{**c.__dict__, "batch_size": 6})
+    ds = make_ds(g["patterns"], g["positions_in"], g["window"])
+    st = pk.initialize(ds, cfg)
+    for _ in range(2):
+        pk.sweep(st, ds, cfg, group=dist.group.WORLD if world > 1 else None)
+    if rank == 0:
+        q.put((st.obj.cpu().numpy(), st.probe_stack.cpu().numpy(), list(st.error_trace)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _spawn(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_run, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return out
+
+
+def test_two_rank_batched_sweep_matches_one_rank(gpu):
+    one = _spawn(1)
+    two = _spawn(2)
+    scale = np.linalg.norm(one[0])
+    assert np.linalg.norm(two[0] - one[0]) / scale < 1e-12
+    assert np.linalg.norm(two[1] - one[1]) / np.linalg.norm(one[1]) < 1e-12
+    np.testing.assert_allclose(two[2], one[2], rtol=1e-12)
