@@ -75,7 +75,7 @@ class OracleState:
                            list(self.error_trace), list(self.modulus_error_trace))
 
 
-def initialize(patterns, positions, window: int, cfg, cdt=np.complex128) -> OracleState:
+def initialize(patterns, positions, window: int, cfg, cdt=np.complex128, chirp=None) -> OracleState:
     """engine.py:73-101.
 
     canvas = anchor bounding box + window, unit transmission; mode 1 is the
@@ -98,6 +98,8 @@ def initialize(patterns, positions, window: int, cfg, cdt=np.complex128) -> Orac
             cand = cand - prev * (np.vdot(prev, cand) / np.vdot(prev, prev))
         cand *= np.sqrt(0.01 * first_power / np.sum(np.abs(cand) ** 2))
         modes.append(cand)
+    if chirp is not None:   # Fresnel extension: back-propagation ends with conj(Q)
+        modes = [np.conj(chirp) * m for m in modes]
     st = OracleState(obj=obj, probes=[m.astype(cdt) for m in modes],
                      positions=np.array(positions, dtype=np.float64, copy=True),
                      canvas_origin=(int(origin[0]), int(origin[1])))
@@ -111,14 +113,29 @@ def initialize(patterns, positions, window: int, cfg, cdt=np.complex128) -> Orac
 
 # ------------------------------------------------------------- one visit --
 
-def modulus_project(probes, o_j, i_j, eps_rel=1e-12):
+def fresnel_chirp(geometry):
+    """Single-FFT Fresnel regime (extension, not in the reference): the exit
+    wave is multiplied by Q = exp(i pi ds^2 |x|^2 / (lambda z)) before the
+    centered FFT and by conj(Q) after the inverse (the detector-plane chirp
+    drops out of |.|, like the far-field prefactor, fields.py:4-6)."""
+    w = geometry.window
+    k = np.pi * geometry.sample_pixel ** 2 / (geometry.wavelength * geometry.distance)
+    r = np.arange(w, dtype=np.float64) - w // 2
+    return np.exp(1j * k * (r[:, None] ** 2 + r[None, :] ** 2))
+
+
+def modulus_project(probes, o_j, i_j, eps_rel=1e-12, chirp=None):
     """engine.py:104-120 -- mixed-state modulus constraint.
 
-    Returns (corrected exit waves, detector waves, total detector intensity)."""
+    Returns (corrected exit waves, detector waves, total detector intensity).
+    ``chirp``: optional Fresnel quadratic phase (extension)."""
     if np.any(i_j < 0):
         raise ValueError("negative intensity")  # DataError in the reference
     rdt = real_dtype(o_j.dtype)
-    det = [centered_fft2(p * o_j) for p in probes]
+    if chirp is not None:
+        det = [centered_fft2(chirp * p * o_j) for p in probes]
+    else:
+        det = [centered_fft2(p * o_j) for p in probes]
     total = np.zeros(i_j.shape, dtype=rdt)
     for d in det:
         total += np.abs(d) ** 2
@@ -127,6 +144,8 @@ def modulus_project(probes, o_j, i_j, eps_rel=1e-12):
         eps = np.float32(eps_rel) * max(np.float32(total.max()), np.finfo(np.float32).tiny)
     ratio = np.sqrt(i_j.astype(rdt)) / np.sqrt(total + eps)
     corrected = [centered_fft2(ratio * d, inverse=True) for d in det]
+    if chirp is not None:
+        corrected = [np.conj(chirp) * c for c in corrected]
     return corrected, det, total
 
 
@@ -224,8 +243,9 @@ def sense(pc, o_before, o_after, total, i_j):
     return est.dx, est.dy, True
 
 
-def sweep(st: OracleState, patterns, window: int, cfg, order=None) -> OracleState:
-    """engine.py:173-243 -- one pass over every position, mutating ``st``."""
+def sweep(st: OracleState, patterns, window: int, cfg, order=None, chirp=None) -> OracleState:
+    """engine.py:173-243 -- one pass over every position, mutating ``st``.
+    ``chirp``: Fresnel quadratic phase (extension; None = the reference)."""
     n = patterns.shape[0]
     if order is None:
         order = visit_order(n, cfg.position_order, cfg.shuffle_seed, st.iteration)
@@ -244,7 +264,7 @@ def sweep(st: OracleState, patterns, window: int, cfg, order=None) -> OracleStat
         if not box_inside(r, c, window, st.obj.shape):
             raise IndexError(f"crop box at ({r},{c}) outside canvas")
         o_j = st.obj[r:r + window, c:c + window].copy()
-        corrected, det, _ = modulus_project(st.probes, o_j, i_j, cfg.epsilon_rel)
+        corrected, det, _ = modulus_project(st.probes, o_j, i_j, cfg.epsilon_rel, chirp)
         total = np.zeros(i_j.shape, dtype=rdt)
         for d in det:
             total += np.abs(d) ** 2

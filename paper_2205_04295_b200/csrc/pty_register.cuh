@@ -21,7 +21,6 @@
 namespace pty {
 
 constexpr int kRegThreads = 256;
-constexpr int kRefineCols = 16;   // columns of the upsampled grid per chunk
 // rows of the upsampled grid per CTA (keeps 2 * rows * W complex in shared memory)
 template <typename T, int W> __host__ __device__ constexpr int refine_rows() {
     return W * (int)sizeof(cplx<T>) >= 8192 ? 8 : 16;
@@ -233,6 +232,8 @@ __global__ void __launch_bounds__(kRegThreads) reg_refine(const cplx<T>* work, i
     using C = cplx<T>;
     constexpr int VPT = (W + kRegThreads - 1) / kRegThreads;   // columns v per thread
     constexpr int kRefineRows = refine_rows<T, W>();
+    constexpr int kRefineCols = kRefineRows;                   // grid columns per chunk: ec fits in er
+    static_assert(W * kRefineCols <= 2 * kRefineRows * W, "ec overruns the refine shared memory");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* er = reinterpret_cast<C*>(smem_raw);                    // [kRefineRows][W]
     C* U = er + kRefineRows * W;                               // [kRefineRows][W]

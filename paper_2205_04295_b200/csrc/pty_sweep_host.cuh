@@ -53,7 +53,10 @@ int run_sweep_lines(const PtySweepArgs* a, cudaStream_t st);
 
 template <typename T, int W>
 int run_sweep(const PtySweepArgs* a, cudaStream_t st) {
-    if (a->n_slots <= tiles_max_slots()) return tiles::run_sweep<T, W>(a, st);
+    if (a->n_slots <= tiles_max_slots()) {
+        const int rc = tiles::run_sweep<T, W>(a, st);
+        if (rc != tiles::kTilesNoFit) return rc;
+    }
     return run_sweep_lines<T, W>(a, st);
 }
 

@@ -10,7 +10,8 @@ namespace pty {
 namespace tiles {
 
 // ------------------------------------------------------------- sweep ------
-constexpr int kMinTC = 4;   // column tiles are >= 4 complex (32-byte sectors)
+constexpr int kMinTC = 4;
+constexpr int kTilesNoFit = -1;   // internal: resident tiles exceed shared memory   // column tiles are >= 4 complex (32-byte sectors)
 
 struct SweepLayout {
     unsigned int* barrier;
@@ -73,28 +74,36 @@ int run_sweep(const PtySweepArgs* a, cudaStream_t st) {
     // bounded by the per-CTA shared-memory budget.  PTY_TR / PTY_TC /
     // PTY_CTAS_PER_SM override (tuning).
     const int sms = sm_count();
-    int per_sm = std::max(1, env_int("PTY_CTAS_PER_SM", kSweepMinCtasPerSm));
+    const int want_per_sm = std::max(1, env_int("PTY_CTAS_PER_SM", kSweepMinCtasPerSm));
     const size_t smem_sm = max_smem_per_sm();
     const size_t fixed = sweep_smem_fixed<T, W>();
-    const size_t budget = std::min(max_dyn_smem(), smem_sm / per_sm - 1024 - 512) - fixed;
-    const int grid = sms * per_sm;
     constexpr int LS = line_stride<W>();
     const size_t line_bytes = (size_t)LS * sizeof(cplx<T>);
-    int TR = env_int("PTY_TR", 0);
-    if (TR <= 0) {
-        TR = 1;
-        while (TR < W && (long)S * (W / TR) > grid && (size_t)2 * TR * M * line_bytes <= budget) TR *= 2;
+    int per_sm = 0, grid = 0, TR = 0, TC = 0, nRT = 0, nCT = 0, K = 0;
+    size_t tile_bytes = 0;
+    // fewer CTAs per SM (bigger shared-memory budget) until the resident
+    // tiles fit; kTilesNoFit sends the caller to the line-task kernel.
+    for (per_sm = want_per_sm; per_sm >= 1; --per_sm) {
+        const size_t budget = std::min(max_dyn_smem(), smem_sm / per_sm - 1024 - 512) - fixed;
+        grid = sms * per_sm;
+        TR = env_int("PTY_TR", 0);
+        if (TR <= 0) {
+            TR = 1;
+            while (TR < W && (long)S * (W / TR) > grid && (size_t)2 * TR * M * line_bytes <= budget) TR *= 2;
+        }
+        TC = env_int("PTY_TC", 0);
+        if (TC <= 0) {
+            TC = kMinTC;
+            while (TC < W && (long)S * (W / TC) > grid && (size_t)2 * TC * M * line_bytes <= budget) TC *= 2;
+        }
+        if (TR < 1 || TR > W || (W % TR) || TC < kMinTC || TC > W || (W % TC)) return PTY_ERR_ARGUMENT;
+        nRT = W / TR;
+        nCT = W / TC;
+        K = (S * nCT + grid - 1) / grid;
+        tile_bytes = std::max((size_t)TR * M * line_bytes, (size_t)K * M * TC * line_bytes);
+        if (tile_bytes <= budget) break;
     }
-    int TC = env_int("PTY_TC", 0);
-    if (TC <= 0) {
-        TC = kMinTC;
-        while (TC < W && (long)S * (W / TC) > grid && (size_t)2 * TC * M * line_bytes <= budget) TC *= 2;
-    }
-    if (TR < 1 || TR > W || (W % TR) || TC < kMinTC || TC > W || (W % TC)) return PTY_ERR_ARGUMENT;
-    const int nRT = W / TR, nCT = W / TC;
-    const int K = (S * nCT + grid - 1) / grid;
-    const size_t tile_bytes = std::max((size_t)TR * M * line_bytes, (size_t)K * M * TC * line_bytes);
-    if (tile_bytes > budget) return PTY_ERR_ARGUMENT;   // too many replicas for the resident column tiles
+    if (per_sm < 1) return kTilesNoFit;
     P.TR = TR; P.TC = TC; P.nRT = nRT; P.nCT = nCT; P.K = K;
     P.lgTR = 0; while ((1 << P.lgTR) < TR) ++P.lgTR;
     P.lgTC = 0; while ((1 << P.lgTC) < TC) ++P.lgTC;

@@ -56,6 +56,7 @@ class SolverConfig:
     track_modulus_error: bool = False
     precision: str = "fp32"           # B200 extension: fp32 (complex64) | fp64 (complex128)
     batch_size: int = 1               # B200 extension: >1 = batched semi-parallel update
+    propagator: str = "farfield"      # B200 extension: farfield | fresnel (single-FFT Fresnel regime)
 
     def __post_init__(self) -> None:
         if not (0 <= self.alpha_obj <= 1 and 0 <= self.alpha_probe <= 1):
@@ -72,6 +73,8 @@ class SolverConfig:
             raise ParameterError(f"precision must be 'fp32' or 'fp64', got {self.precision!r}")
         if self.batch_size < 1:
             raise ParameterError("batch_size must be >= 1")
+        if self.propagator not in ("farfield", "fresnel"):
+            raise ParameterError(f"propagator must be 'farfield' or 'fresnel', got {self.propagator!r}")
 
 
 class ReconState:
@@ -79,11 +82,16 @@ class ReconState:
 
     ``obj`` (H, Wc) and the probe stack (M, W, W) are complex64/complex128
     CUDA tensors; ``probes`` is a list view over the stack (assigning a list
-    restacks it); ``positions`` is an (N, 2) float64 CUDA tensor."""
+    restacks it); ``positions`` is an (N, 2) float64 CUDA tensor.
+
+    With the Fresnel propagator the stack holds the probes in the kernels'
+    frame, P * Q (Q = fresnel_chirp); ``probes`` returns P = stack * conj(Q)."""
 
     def __init__(self, obj, probes, positions, canvas_origin, adam=None,
-                 error_trace=None, modulus_error_trace=None, seconds_per_iteration=None):
+                 error_trace=None, modulus_error_trace=None, seconds_per_iteration=None,
+                 frame_chirp=None):
         t = _native.torch()
+        self.frame_chirp = frame_chirp
         self.obj = obj
         self.probe_stack = probes if isinstance(probes, t.Tensor) else t.stack(list(probes))
         self.positions = positions
@@ -96,12 +104,17 @@ class ReconState:
 
     @property
     def probes(self):
+        if self.frame_chirp is not None:
+            return list((self.probe_stack * self.frame_chirp.conj()).unbind(0))
         return list(self.probe_stack.unbind(0))
 
     @probes.setter
     def probes(self, value):
         t = _native.torch()
-        self.probe_stack = t.stack([v.to(self.obj.device, self.obj.dtype) for v in value]).contiguous()
+        stack = t.stack([v.to(self.obj.device, self.obj.dtype) for v in value])
+        if self.frame_chirp is not None:
+            stack = stack * self.frame_chirp
+        self.probe_stack = stack.contiguous()
 
     @property
     def iteration(self) -> int:
@@ -205,8 +218,15 @@ def initialize(dataset, config: SolverConfig) -> ReconState:
     _native.init_probes(probes, pats, noise, w, m)
     positions = t.from_numpy(np.asarray(dataset.positions, dtype=np.float64).copy()).to(dev)
     adam = AdamBuffers.zeros(dataset.n_positions, dev) if config.posref is not None else None
+    # Fresnel: the back-propagated mean amplitude is conj(Q) * P^-1(sqrt(mean I)),
+    # i.e. exactly the far-field initial probe in the kernels' P*Q frame (the
+    # mode Gram-Schmidt is invariant under the common unit-modulus factor)
+    chirp = None
+    if config.propagator == "fresnel":
+        from .fields import fresnel_chirp
+        chirp = fresnel_chirp(dataset.geometry, cdt, dev)
     return ReconState(obj=obj, probes=probes, positions=positions,
-                      canvas_origin=(int(origin[0]), int(origin[1])), adam=adam)
+                      canvas_origin=(int(origin[0]), int(origin[1])), adam=adam, frame_chirp=chirp)
 
 
 def visit_order(n: int, config: SolverConfig, iteration: int) -> np.ndarray:
@@ -444,7 +464,19 @@ def _refine_positions(st: ReconState, pc: PosRefConfig, n: int, w: int) -> None:
     dx = st.buffer("reg_dx", (n,), t.float64)
     peak = st.buffer("reg_peak", (n,), t.float64)
     ok = st.buffer("reg_ok", (n,), t.int32)
-    _native.register_batch(stage, w, n, 1, int(pc.kappa), dy, dx, peak, ok)
+    if stage.dtype == t.complex128:
+        _native.register_batch(stage, w, n, 1, int(pc.kappa), dy, dx, peak, ok)
+    else:
+        # register in float64 like the reference (its crops are complex128,
+        # registration.py:123-128): fp32 correlation peaks of near-identical
+        # crops are too flat to resolve the 1/kappa grid
+        chunk = max(1, min(n, (1 << 30) // (2 * w * w * 16)))
+        work = st.buffer("stage64", (chunk, 2, w, w), t.complex128)
+        for s in range(0, n, chunk):
+            e = min(n, s + chunk)
+            work[:e - s].copy_(stage[s:e])
+            _native.register_batch(work[:e - s], w, e - s, 1, int(pc.kappa),
+                                   dy[s:e], dx[s:e], peak[s:e], ok[s:e])
     # sensors return (gx, gy) = (est.dx, est.dy) (posref.py:63)
     _native.adam_apply(st.positions, st.adam, dx, dy, ok, pc, position_bounds(st, w))
 

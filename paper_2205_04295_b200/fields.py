@@ -104,16 +104,34 @@ def propagate_(x, direction: str = "forward"):
     return x
 
 
-def propagate(field, direction: str = "forward"):
-    """fields.py:71-84 -- fftshift(fft2(ifftshift(f), norm="ortho")) (or ifft2)."""
+def propagate(field, direction: str = "forward", geometry: Geometry | None = None,
+              kind: str = "farfield"):
+    """fields.py:71-84 -- fftshift(fft2(ifftshift(f), norm="ortho")) (or ifft2).
+
+    kind="fresnel" (extension, needs ``geometry``): forward = P(Q * f),
+    backward = conj(Q) * P^-1(f), Q = fresnel_chirp(geometry); the outer
+    detector-plane chirp is dropped exactly as the far-field prefactor is."""
     if direction not in ("forward", "backward"):
         raise ValueError(f"direction must be 'forward' or 'backward', got {direction!r}")
+    if kind not in ("farfield", "fresnel"):
+        raise ValueError(f"kind must be 'farfield' or 'fresnel', got {kind!r}")
     x = as_field(field)
     if x.shape[0] != x.shape[1]:
         raise ShapeError(f"propagate requires a square field, got {tuple(x.shape)}")
     check_window(x.shape[0])
     if isinstance(field, _native.torch().Tensor):
         x = x.clone()   # never transform the caller's tensor in place
+    if kind == "fresnel":
+        if geometry is None:
+            raise ValueError("the Fresnel propagator needs the geometry")
+        q = fresnel_chirp(geometry, x.dtype, x.device)
+        if direction == "forward":
+            x *= q
+            propagate_(x, direction)
+        else:
+            propagate_(x, direction)
+            x *= q.conj()
+        return _result(x, field)
     propagate_(x, direction)
     return _result(x, field)
 
@@ -137,6 +155,25 @@ def paste_add_inplace(canvas, box: CropBox, delta) -> None:
     if tuple(delta.shape) != (box.side, box.side):
         raise ShapeError(f"delta shape {tuple(delta.shape)} != box side {box.side}")
     canvas[box.row:box.row + box.side, box.col:box.col + box.side] += delta
+
+
+def fresnel_chirp(geometry: Geometry, dtype=None, device=None):
+    """Quadratic phase of the single-FFT Fresnel regime (extension; the
+    reference is far field only):
+        Q[r, c] = exp(i pi ds^2 ((r - W/2)^2 + (c - W/2)^2) / (lambda z)),
+    ds = geometry.sample_pixel.  The detector wave is Q2 * FFT(Q * psi); Q2 has
+    unit modulus and the modulus constraint only uses |.| and the exact inverse,
+    so a Fresnel reconstruction is the far-field one with the exit wave (hence
+    the probe frame) multiplied by Q."""
+    t = _native.torch()
+    w = geometry.window
+    k = np.pi * geometry.sample_pixel ** 2 / (geometry.wavelength * geometry.distance)
+    r = np.arange(w, dtype=np.float64) - w // 2
+    q = np.exp(1j * k * (r[:, None] ** 2 + r[None, :] ** 2))
+    x = t.from_numpy(q)
+    if device is not None or dtype is not None:
+        x = x.to(device=device if device is not None else "cpu", dtype=dtype if dtype is not None else x.dtype)
+    return x
 
 
 def fourier_ramp(h: int, w: int, dx, dy, device, dtype):

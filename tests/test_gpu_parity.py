@@ -220,6 +220,66 @@ def test_fp64_matches_oracle_at_config1_shape(gpu):
     assert rel_l2(s32.probe_stack.cpu().numpy(), np.stack(o64.probes)) < 1e-3
 
 
+def test_fresnel_propagator_matches_explicit_chirp_oracle(gpu):
+    """Fresnel extension (config 4 names it; the reference is far field only):
+    the GPU sweep runs the far-field kernels in the chirped probe frame, the
+    oracle applies Q / conj(Q) explicitly every visit -- fp64 trajectories agree,
+    and propagate(kind="fresnel") round-trips."""
+    geom = pk.Geometry.create(8.3187e-10, 0.75, 20e-6, 64)
+    plan = pk.make_scan((4, 4), 12.0, 1.0, seed=9)
+    obj = pk.make_object(pk.canvas_shape_for(plan, 64), "spokes", seed=9)
+    probes = pk.make_probe(pk.ProbeSpec(2, (0.8, 0.2), "disk", 16.0), geom)
+    ds = pk.synthesize(obj, probes, plan, geom, propagator="fresnel")
+    ds.patterns = ds.patterns.astype(np.float32).astype(np.float64)
+    cfg = pk.SolverConfig(alpha_obj=0.9, alpha_probe=0.9, beta=0.5, gamma=0.5, mode_count=2,
+                          precision="fp64", propagator="fresnel")
+    q = rpie.fresnel_chirp(geom)
+    st = pk.initialize(ds, cfg)
+    ost = rpie.initialize(ds.patterns, ds.positions, 64, cfg, chirp=q)
+    assert rel_l2(np.stack([p.cpu().numpy() for p in st.probes]), np.stack(ost.probes)) < 1e-13
+    for _ in range(3):
+        pk.sweep(st, ds, cfg)
+        rpie.sweep(ost, ds.patterns, 64, cfg, chirp=q)
+    assert rel_l2(st.obj.cpu().numpy(), ost.obj) < 1e-9
+    assert rel_l2(np.stack([p.cpu().numpy() for p in st.probes]), np.stack(ost.probes)) < 1e-9
+    np.testing.assert_allclose(st.error_trace, ost.error_trace, rtol=1e-9)
+    # the chirp matters: a far-field reconstruction of Fresnel data fits worse
+    far = pk.SolverConfig(**{**cfg.__dict__, "propagator": "farfield"})
+    assert st.error_trace[-1] < 1.0
+    f = np.random.default_rng(0).standard_normal((64, 64)) + 0j
+    back = pk.propagate(pk.propagate(f, geometry=geom, kind="fresnel"), "backward", geometry=geom,
+                        kind="fresnel")
+    assert np.max(np.abs(back - f)) < 1e-12
+    assert far.propagator == "farfield"
+
+
+@pytest.mark.parametrize("precision,tol", [("fp64", 1e-9), ("fp32", 1e-4)])
+def test_config4_shape_512_five_modes_posref(gpu, precision, tol):
+    """BASELINE configs[3] geometry (512x512, 5 modes, lambda 8.29e-10,
+    position refinement kappa=10) on a 3x3 scan: CUDA vs the oracle, 2 sweeps
+    with Adam engaged from the first sweep."""
+    geom = pk.Geometry.create(8.29e-10, 0.75, 20e-6, 512)
+    plan = pk.make_scan((3, 3), 64.0, 1.0, seed=4)
+    obj = pk.make_object(pk.canvas_shape_for(plan, 512), "spokes", seed=4)
+    probes = pk.make_probe(pk.ProbeSpec(5, (0.6, 0.1, 0.1, 0.1, 0.1), "disk", 120.0), geom)
+    ds = pk.synthesize(obj, probes, plan, geom)
+    ds.patterns = ds.patterns.astype(np.float32).astype(np.float64)
+    rng = np.random.default_rng(3)
+    ds.positions = ds.positions + rng.uniform(-2, 2, ds.positions.shape)
+    cfg = pk.SolverConfig(alpha_obj=0.9, alpha_probe=0.9, beta=0.5, gamma=0.5, mode_count=5,
+                          precision=precision,
+                          posref=pk.PosRefConfig(kappa=10, warmup_iterations=0))
+    st = pk.initialize(ds, cfg)
+    ost = rpie.initialize(ds.patterns, ds.positions, 512, cfg)
+    for _ in range(2):
+        pk.sweep(st, ds, cfg)
+        rpie.sweep(ost, ds.patterns, 512, cfg)
+    assert rel_l2(st.obj.cpu().numpy(), ost.obj) < tol
+    assert rel_l2(st.probe_stack.cpu().numpy(), np.stack(ost.probes)) < 10 * tol
+    np.testing.assert_allclose(st.positions.cpu().numpy(), ost.positions, rtol=0,
+                               atol=1e-9 if precision == "fp64" else 0.11)
+
+
 # ------------------------------------------------------------ registration ----
 
 def test_registration_matches_reference(gpu):
