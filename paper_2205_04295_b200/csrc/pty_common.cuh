@@ -28,6 +28,45 @@ template <typename T> __device__ __forceinline__ cplx<T> mulc(cplx<T> a, cplx<T>
 }
 template <typename T> __device__ __forceinline__ cplx<T> scale(cplx<T> a, T s) { return {a.re * s, a.im * s}; }
 template <typename T> __device__ __forceinline__ cplx<T> conjg(cplx<T> a) { return {a.re, -a.im}; }
+
+// complex<float> on the sm_100 packed-fp32 pipe: one FADD2 / FMUL2 / FFMA2
+// per complex add, sub and real scale instead of two scalar instructions
+// (same IEEE round-to-nearest result per component, no contraction).
+__device__ __forceinline__ unsigned long long f2pack(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ cplx<float> f2unpack(unsigned long long r) {
+    cplx<float> a;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a.re), "=f"(a.im) : "l"(r));
+    return a;
+}
+__device__ __forceinline__ cplx<float> operator+(cplx<float> a, cplx<float> b) {
+    unsigned long long z;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(z) : "l"(f2pack(a.re, a.im)), "l"(f2pack(b.re, b.im)));
+    return f2unpack(z);
+}
+__device__ __forceinline__ cplx<float> operator-(cplx<float> a, cplx<float> b) {
+    unsigned long long z;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(z) : "l"(f2pack(a.re, a.im)), "l"(f2pack(b.re, b.im)));
+    return f2unpack(z);
+}
+__device__ __forceinline__ cplx<float> scale(cplx<float> a, float s) {
+    unsigned long long z;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(z) : "l"(f2pack(a.re, a.im)), "l"(f2pack(s, s)));
+    return f2unpack(z);
+}
+// x * (c + i s) for a compile-time twiddle: c*(xr, xi) + (xi, xr)*(-s, s)
+__device__ __forceinline__ cplx<float> rot_const(cplx<float> x, float c, float s) {
+    unsigned long long t, z;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(f2pack(x.re, x.im)), "l"(f2pack(c, c)));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(z) : "l"(f2pack(x.im, x.re)), "l"(f2pack(-s, s)), "l"(t));
+    return f2unpack(z);
+}
+template <typename T> __device__ __forceinline__ cplx<T> rot_const(cplx<T> x, T c, T s) {
+    return {x.re * c - x.im * s, x.re * s + x.im * c};
+}
 template <typename T> __device__ __forceinline__ T norm2(cplx<T> a) { return a.re * a.re + a.im * a.im; }
 // numpy's complex / real: Smith's rule with a zero imaginary divisor reduces
 // to a multiply by the reciprocal (numpy loops_arithm_fp complex divide).
@@ -35,6 +74,12 @@ template <typename T> __device__ __forceinline__ cplx<T> divr(cplx<T> a, T d) {
     T inv = T(1) / d;
     return {a.re * inv, a.im * inv};
 }
+
+// Hide a value from loop-invariant code motion: the compiler otherwise hoists
+// per-element reciprocals out of the mode loop and spills them to local
+// memory (measured: the reload stalls dominated the row-update phase).
+__device__ __forceinline__ void opaque(float& x) { asm volatile("" : "+f"(x)); }
+__device__ __forceinline__ void opaque(double& x) { asm volatile("" : "+d"(x)); }
 
 template <typename T> struct real_limits;
 template <> struct real_limits<float>  { static __device__ __forceinline__ float tiny() { return 1.17549435e-38f; } };

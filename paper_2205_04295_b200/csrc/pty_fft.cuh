@@ -65,7 +65,7 @@ __device__ __forceinline__ cplx<T> twiddle32(cplx<T> x, int j) {
     if (j == 24) return INV ? cplx<T>{x.im, -x.re} : cplx<T>{-x.im, x.re};
     const T c = T(cos32(j));
     const T s = INV ? T(sin32(j)) : T(-sin32(j));
-    return {x.re * c - x.im * s, x.re * s + x.im * c};
+    return rot_const<T>(x, c, s);
 }
 
 // In-register DFT of N <= 32 points, natural order in and out (radix-2 DIT).

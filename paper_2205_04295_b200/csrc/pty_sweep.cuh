@@ -121,7 +121,34 @@ __device__ __forceinline__ T cta_max_of(const T* p, int n, T* cell) {
 // and the four phases, one method per
 // phase body; they are inlined (non-inlined member calls spill the CTA state
 // to local memory, measured 2x slower).
-template <typename T, int W>
+//
+// CL = false: one cooperative grid walks every slot in lock-step, phases
+// separated by the software grid barrier.  CL = true: one thread-block cluster
+// per slot (grid = nslots x clusterDim), phases separated by the hardware
+// cluster barrier; slots run independently, so one slot's barrier wait is
+// covered by another slot's CTAs on the same SM.
+__device__ __forceinline__ unsigned cluster_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ unsigned cluster_size() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ unsigned cluster_index() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+    return r;
+}
+// all threads of all CTAs of the cluster; release/acquire at cluster scope
+// orders the global-memory scratch traffic between phases
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <typename T, int W, bool CL>
 __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kernel(const __grid_constant__ SweepDev P) {
     using C = cplx<T>;
     constexpr int B = Shape<W>::B, TEAM = 4 * B, XS = xch_size<W>(), LS4 = team_line_stride<W>();
@@ -134,7 +161,12 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
     unsigned char* region = smem_raw + sweep_smem_fixed<T, W>();
 
     const int tid = threadIdx.x, NT = blockDim.x;
-    const int M = P.M, N = P.N, S = P.nslots;
+    const int M = P.M, N = P.N;
+    // slot range and CTA coordinates of this kernel flavour
+    const int s0 = CL ? (int)cluster_index() : 0;
+    const int S = CL ? 1 : P.nslots;                       // slots walked by this CTA set
+    const int cta = CL ? (int)cluster_rank() : (int)blockIdx.x;
+    const int ncta = CL ? (int)cluster_size() : (int)gridDim.x;
     const size_t WW = (size_t)W * W;
     const int nq = W / 4;
     const int team = tid / TEAM, tl = tid % TEAM, gi = tl / B, b = tid % B, grp = tid / B;
@@ -159,10 +191,15 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
                  (size_t)2 * NTEAM * 4 * W + team * 4;
 
     GridBarrier bar{P.barrier, 0u};
+    auto phase_sync = [&]() {
+        if constexpr (CL) cluster_sync();
+        else bar.sync();
+    };
     load_twiddles<T, W>(tw, reinterpret_cast<const C*>(P.twiddles));
 
     // ---- phase 0: anchors (engine.py:69-70, 192-195) + bounds, initial probe peak
-    for (int idx = blockIdx.x * NT + tid; idx < S * N; idx += gridDim.x * NT) {
+    for (int li = cta * NT + tid; li < S * N; li += ncta * NT) {
+        const int idx = s0 * N + li;
         const int s = idx / N, j = idx % N;
         const SlotDev& sl = P.slot[s];
         const double x = sl.positions[2 * j], y = sl.positions[2 * j + 1];
@@ -172,8 +209,8 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
         P.anchors[2 * idx + 1] = ac;
         if (ar < 0 || ac < 0 || ar + W > sl.H || ac + W > sl.Wc) atomicOr(sl.status, PTY_ERR_BOUNDS);
     }
-    for (int item = blockIdx.x; item < S * nq; item += gridDim.x) {
-        const int s = item / nq, rq = item % nq;
+    for (int item = cta; item < S * nq; item += ncta) {
+        const int s = s0 + item / nq, rq = item % nq;
         const C* probes = reinterpret_cast<const C*>(P.slot[s].probes);
         T pk = T(0);
         for (int i = tid; i < 4 * W; i += NT) {
@@ -185,7 +222,7 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
         pk = block_max(pk, red);
         if (tid == 0) peak_part[(size_t)s * nq + rq] = pk;
     }
-    bar.sync();
+    phase_sync();
 
     auto stamp = [&](int step, int k) {
         if (P.timeline && step < P.timeline_steps) {
@@ -196,17 +233,18 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
     for (int step = 0; step < N; ++step) {
         stamp(step, 0);
         if (tid < S) {   // status only changes in P4 / phase 0, both behind a barrier
-            const SlotDev& sl = P.slot[tid];
+            const int s = s0 + tid;
+            const SlotDev& sl = P.slot[s];
             const int j = sl.order[step];
-            s_dead[tid] = *(volatile const int*)sl.status;
-            s_j[tid] = j;
-            s_ar[tid] = P.anchors[2 * (tid * N + j)];
-            s_ac[tid] = P.anchors[2 * (tid * N + j) + 1];
+            s_dead[s] = *(volatile const int*)sl.status;
+            s_j[s] = j;
+            s_ar[s] = P.anchors[2 * (s * N + j)];
+            s_ac[s] = P.anchors[2 * (s * N + j) + 1];
         }
         __syncthreads();
         // ---------------------------------------------------------- P1 rows
-        for (int task = blockIdx.x * NTEAM + team; task < S * M * nq; task += gridDim.x * NTEAM) {
-            const int s = task / (M * nq), m = (task / nq) % M, rq = task % nq;
+        for (int task = cta * NTEAM + team; task < S * M * nq; task += ncta * NTEAM) {
+            const int s = s0 + task / (M * nq), m = (task / nq) % M, rq = task % nq;
             if (s_dead[s]) continue;
             const SlotDev& sl = P.slot[s];
             const int j = s_j[s];
@@ -224,19 +262,19 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
             if (m == 0 && tl == 0) omax_part[(size_t)s * nq + rq] = om;
         }
         stamp(step, 1);
-        bar.sync();
+        phase_sync();
         // ------------------------------------------------- P2 cols (forward)
-        for (int task = blockIdx.x * NGRP + grp; task < S * W; task += gridDim.x * NGRP) {
-            const int s = task / W, kc = task % W;
+        for (int task = cta * NGRP + grp; task < S * W; task += ncta * NGRP) {
+            const int s = s0 + task / W, kc = task % W;
             if (s_dead[s]) continue;
             const T tm = task_col_fwd<T, W>(tw, xch, b, gmask, scratch + (size_t)s * M * WW, M, kc, totT + (size_t)s * WW);
             if (b == 0) tmax_part[(size_t)s * W + kc] = tm;
         }
         stamp(step, 2);
-        bar.sync();
+        phase_sync();
         // ---------------------------------------- P3 modulus + cols (inverse)
-        for (int task = blockIdx.x * NGRP + grp; task < S * W; task += gridDim.x * NGRP) {
-            const int s = task / W, kc = task % W;
+        for (int task = cta * NGRP + grp; task < S * W; task += ncta * NGRP) {
+            const int s = s0 + task / W, kc = task % W;
             if (s_dead[s]) continue;
             const SlotDev& sl = P.slot[s];
             const int j = s_j[s];
@@ -247,16 +285,17 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
                                P.err_part + (((size_t)s * N + step) * W + kc) * 3);
         }
         stamp(step, 3);
-        bar.sync();
+        phase_sync();
         // --------------------------------------- P4 rows (inverse) + update
-        for (int task = blockIdx.x * NTEAM + team; task < S * nq; task += gridDim.x * NTEAM) {
-            const int s = task / nq, rq = task % nq;
+        for (int task = cta * NTEAM + team; task < S * nq; task += ncta * NTEAM) {
+            const int s = s0 + task / nq, rq = task % nq;
             if (s_dead[s]) continue;
             const SlotDev& sl = P.slot[s];
             const int j = s_j[s];
-            const T* pkp = peak_part + ((size_t)(step & 1) * S + s) * nq;
+            const T* pkp = peak_part + ((size_t)(step & 1) * P.nslots + s) * nq;
             const T* omp = omax_part + (size_t)s * nq;
             T peak = T(0), omax = T(0);
+#pragma unroll
             for (int q = b; q < nq; q += B) {
                 peak = fmax(peak, pkp[q]);
                 omax = fmax(omax, omp[q]);
@@ -276,10 +315,10 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
                                                     scratch + (size_t)s * M * WW, M, rq, reinterpret_cast<C*>(sl.obj),
                                                     sl.Wc, s_ar[s], s_ac[s], reinterpret_cast<C*>(sl.probes), peak,
                                                     omax, U, stg);
-            if (tl == 0) peak_part[((size_t)((step + 1) & 1) * S + s) * nq + rq] = npk;
+            if (tl == 0) peak_part[((size_t)((step + 1) & 1) * P.nslots + s) * nq + rq] = npk;
         }
         stamp(step, 4);
-        bar.sync();
+        phase_sync();
     }
 }
 

@@ -88,20 +88,53 @@ int run_sweep_lines(const PtySweepArgs* a, cudaStream_t st) {
         outs.p[s] = h.err_out;
     }
 
-    // launch geometry: kSweepThreads-thread CTAs, as many per SM as fit (<= 2),
-    // cooperative (all co-resident); PTY_CTAS_PER_SM overrides downwards.
+    // launch geometry.  Grid flavour (default): kSweepThreads-thread CTAs, as
+    // many per SM as fit (<= 2), cooperative, all slots in lock-step;
+    // PTY_CTAS_PER_SM overrides downwards.  Cluster flavour (PTY_CLUSTER=K):
+    // one cluster of K CTAs per slot, slots scheduled independently (measured
+    // slower at 16 replicas: 8 clusters of 16 fit the GPCs at once).
     const size_t smem = sweep_smem_fixed<T, W>() + sweep_smem_phase<T, W>(kSweepThreads);
-    auto kern = sweep_kernel<T, W>;
     if (smem > max_dyn_smem()) return PTY_ERR_ARGUMENT;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-        return PTY_ERR_CUDA;
-    int fit = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, kern, kSweepThreads, smem) != cudaSuccess || fit < 1)
-        return PTY_ERR_CUDA;
-    int per_sm = std::min(fit, kSweepMaxCtasPerSm);
-    const int want = env_int("PTY_CTAS_PER_SM", 0);
-    if (want > 0) per_sm = std::min(per_sm, want);
-    const int grid = sm_count() * per_sm;
+    int K = std::max(0, env_int("PTY_CLUSTER", 0));
+    int grid = 0;
+    if (K > 0) {
+        auto kern = sweep_kernel<T, W, true>;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return PTY_ERR_CUDA;
+        if (K > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+            K = 8;
+        // largest power of two <= K with at least one co-resident cluster
+        for (; K >= 1; K /= 2) {
+            cudaLaunchConfig_t cfg{};
+            cudaLaunchAttribute at[1];
+            cfg.gridDim = dim3(K * S);
+            cfg.blockDim = dim3(kSweepThreads);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = st;
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = K;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int nclusters = 0;
+            if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) == cudaSuccess && nclusters > 0) break;
+            cudaGetLastError();
+        }
+        if (K < 1) return PTY_ERR_CUDA;
+        grid = K * S;
+    } else {
+        auto kern = sweep_kernel<T, W, false>;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return PTY_ERR_CUDA;
+        int fit = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, kern, kSweepThreads, smem) != cudaSuccess || fit < 1)
+            return PTY_ERR_CUDA;
+        int per_sm = std::min(fit, kSweepMaxCtasPerSm);
+        const int want = env_int("PTY_CTAS_PER_SM", 0);
+        if (want > 0) per_sm = std::min(per_sm, want);
+        grid = sm_count() * per_sm;
+    }
 
     // debug timeline (PTY_TIMELINE=<steps>): per-CTA phase completion stamps
     const int tl_steps = std::min(env_int("PTY_TIMELINE", 0), N);
@@ -114,8 +147,26 @@ int run_sweep_lines(const PtySweepArgs* a, cudaStream_t st) {
     if (cudaMemsetAsync(L.barrier, 0, sizeof(unsigned int), st) != cudaSuccess) return PTY_ERR_CUDA;
     if (cudaMemsetAsync(L.err_part, 0, (size_t)S * N * W * 3 * sizeof(double), st) != cudaSuccess)
         return PTY_ERR_CUDA;
-    void* args[] = {&P};
-    cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kSweepThreads), args, smem, st);
+    cudaError_t e;
+    if (K > 0) {
+        cudaLaunchConfig_t cfg{};
+        cudaLaunchAttribute at[1];
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kSweepThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = K;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, sweep_kernel<T, W, true>, P);
+    } else {
+        void* args[] = {&P};
+        e = cudaLaunchCooperativeKernel((const void*)sweep_kernel<T, W, false>, dim3(grid), dim3(kSweepThreads), args,
+                                        smem, st);
+    }
     if (e != cudaSuccess) return PTY_ERR_CUDA;
     err_visit_kernel<<<S * N, 256, 0, st>>>(L.err_part, W, L.visit_sum);
     err_slot_kernel<<<S, 256, 0, st>>>(L.visit_sum, N, S, outs);

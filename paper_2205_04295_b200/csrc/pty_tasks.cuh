@@ -98,7 +98,11 @@ __device__ __forceinline__ T task_row_fwd(const cplx<T>* tw, cplx<T>* xch, cplx<
         [&](int kc, int, C v) { tt[kc * 5 + gi] = v; });
     team_sync<TEAM>(team);
     C* dst = dst_pos + m * WW + 4 * rq;
-    for (int e = tl; e < 4 * W; e += TEAM) dst[(size_t)(e >> 2) * W + (e & 3)] = tt[(e >> 2) * 5 + (e & 3)];
+#pragma unroll
+    for (int i = 0; i < 4 * W / TEAM; ++i) {
+        const int e = tl + i * TEAM;
+        dst[(size_t)(e >> 2) * W + (e & 3)] = tt[(e >> 2) * 5 + (e & 3)];
+    }
     T res = T(0);
     if (m == 0) res = team_max4<W>(om, red4, team, gi, b);
     team_sync<TEAM>(team);
@@ -152,7 +156,8 @@ __device__ __forceinline__ void task_col_mod(const cplx<T>* tw, cplx<T>* xch, in
     const size_t WW = (size_t)W * W;
     const T invW2 = T(1) / (T(W) * T(W));
     T tmax = T(0);
-    for (int q = b; q < W; q += B) tmax = fmax(tmax, tmax_pos[q]);
+#pragma unroll
+    for (int i = 0; i < W / B; ++i) tmax = fmax(tmax, tmax_pos[b + i * B]);
     tmax = group_max<B>(tmax);
     const T eps = eps_rel * fmax(tmax, real_limits<T>::tiny());
     const T* It = It_pos + (size_t)kc * W;
@@ -209,8 +214,19 @@ __device__ __forceinline__ void task_col_mod(const cplx<T>* tw, cplx<T>* xch, in
 template <typename T, int W>
 __device__ __forceinline__ void team_load_rows(cplx<T>* lines, const cplx<T>* src_mode, int rq, int tl) {
     constexpr int B = Shape<W>::B, TEAM = 4 * B, LS4 = team_line_stride<W>();
+    constexpr int NE = 4 * W / TEAM;   // elements per thread, all loads in flight before the stores
     const cplx<T>* src = src_mode + 4 * rq;
-    for (int e = tl; e < 4 * W; e += TEAM) lines[(e & 3) * LS4 + pad<W>(e >> 2)] = src[(size_t)(e >> 2) * W + (e & 3)];
+    cplx<T> v[NE];
+#pragma unroll
+    for (int i = 0; i < NE; ++i) {
+        const int e = tl + i * TEAM;
+        v[i] = src[(size_t)(e >> 2) * W + (e & 3)];
+    }
+#pragma unroll
+    for (int i = 0; i < NE; ++i) {
+        const int e = tl + i * TEAM;
+        lines[(e & 3) * LS4 + pad<W>(e >> 2)] = v[i];
+    }
 }
 
 struct UpdateParams {
@@ -269,7 +285,9 @@ __device__ __forceinline__ T task_row_inv_update(const cplx<T>* tw, cplx<T>* lin
                 nrow[c] = nrow[c] + mulc(d, pv[q]);
                 prow_pp[c] += norm2(pv[q]);
                 if (U.update_probe) {
-                    T dp = beta * omax + (T(1) - beta) * norm2(o);
+                    T no2 = norm2(o);
+                    opaque(no2);
+                    T dp = beta * omax + (T(1) - beta) * no2;
                     dp = dp + eps_rel * dmax_p;
                     const C np_ = pv[q] + divr(mulc(scale(d, alpha_p), o), dp);
                     pr[c] = np_;

@@ -431,3 +431,22 @@ def test_posref_engages_only_after_warmup(gpu):
     assert np.array_equal(p0, st.positions.cpu().numpy())
     pk.sweep(st, ds, cfg)
     assert not np.array_equal(p0, st.positions.cpu().numpy())
+
+
+@pytest.mark.parametrize("env", [{"PTY_SWEEP_TILES_MAX": "0", "PTY_CLUSTER": "0"},
+                                 {"PTY_SWEEP_TILES_MAX": "0", "PTY_CLUSTER": "4"}])
+def test_line_task_kernels_match_tile_kernel(gpu, monkeypatch, env):
+    """The line-task sweep (grid and cluster flavours) against the tile sweep:
+    same visit arithmetic, different work decomposition."""
+    g = golden("sweep_rpie")
+    cfg = pkg_cfg(cfg_from_repr(str(g["cfg_repr"])), "fp64")
+    ds = make_ds(g["patterns"], g["positions_in"], g["window"])
+    a = pk.initialize(ds, cfg)
+    pk.sweep(a, ds, cfg)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    b = pk.initialize(ds, cfg)
+    pk.sweep(b, ds, cfg)
+    assert rel_l2(b.obj.cpu().numpy(), a.obj.cpu().numpy()) < 1e-12
+    assert rel_l2(b.probe_stack.cpu().numpy(), a.probe_stack.cpu().numpy()) < 1e-12
+    np.testing.assert_allclose(b.error_trace, a.error_trace, rtol=1e-12)
