@@ -83,18 +83,26 @@ __device__ __forceinline__ T task_row_fwd(const cplx<T>* tw, cplx<T>* xch, cplx<
     const int r = 4 * rq + gi;
     const C* orow = obj + (size_t)(ar + r) * Wc + ac;
     const C* prow = probes + m * WW + (size_t)r * W;
+    constexpr int A = Shape<W>::A;
     C* stg = stg_o ? stg_o + (size_t)r * W : nullptr;
+    // all 2A loads in flight before any use or store (a store between them
+    // would serialise the loads behind it: the pointers may alias)
+    C ov[A], pv[A];
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+        ov[a] = orow[B * a + b];
+        pv[a] = prow[B * a + b];
+    }
     T om = T(0);
+    if (m == 0) {
+#pragma unroll
+        for (int a = 0; a < A; ++a) {
+            om = fmax(om, norm2(ov[a]));
+            if (stg) stg[B * a + b] = ov[a];
+        }
+    }
     group_fft<T, W, false>(
-        xch, tw, b, gmask,
-        [&](int n, int) {
-            const C o = orow[n];
-            if (m == 0) {
-                om = fmax(om, norm2(o));
-                if (stg) stg[n] = o;
-            }
-            return scale(prow[n] * o, checker<T>(r, n));
-        },
+        xch, tw, b, gmask, [&](int n, int a) { return scale(pv[a] * ov[a], checker<T>(r, n)); },
         [&](int kc, int, C v) { tt[kc * 5 + gi] = v; });
     team_sync<TEAM>(team);
     C* dst = dst_pos + m * WW + 4 * rq;
