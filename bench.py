@@ -8,7 +8,11 @@ Workload (BASELINE.json configs[1]): simulated 20x20 scan
 iteration (one sweep over all 400 positions).  Each GPU runs R independent
 reconstructions of that dataset in exact reference (sequential) order,
 interleaved in one cooperative launch per sweep ("replica mode", DESIGN.md);
-R = 1 is the single-reconstruction latency figure, also reported.
+R = 1 is the single-reconstruction latency figure, also reported.  Default
+R = 18: the row-update phase has R * W/4 team tasks and the grid has
+148 SMs x 2 CTAs x 4 teams = 1184 teams, so 18 x 64 = 1152 is the largest R
+that finishes that phase in one round (measured: R = 18 250 K pos/s,
+R = 20 173 K pos/s).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--replicas R]
     python bench.py --impl reference ...   # the reference algorithm on host cores
@@ -410,7 +414,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--replicas", type=int, default=int(os.environ.get("PTY_BENCH_REPLICAS", 16)))
+    ap.add_argument("--replicas", type=int, default=int(os.environ.get("PTY_BENCH_REPLICAS", 18)))
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--cpu-sample", type=int, default=32)
     ap.add_argument("--cpu-workers", type=int, default=0)

@@ -5,7 +5,7 @@ h=rows[hi]; data=[dict(zip(h,r)) for r in rows[hi+1:] if len(r)==len(h)]
 per=collections.defaultdict(dict)
 for d in data:
     per[(d['ID'],d['Kernel Name'].split('(')[0])][d['Metric Name']]=(d['Metric Value'],d['Metric Unit'])
-scale={'byte':1,'Kbyte':1e3,'Mbyte':1e6,'Gbyte':1e9,'nsecond':1e-3,'usecond':1,'msecond':1e3,'second':1e6}
+scale={'ns':1e-3,'us':1,'ms':1e3,'byte':1,'Kbyte':1e3,'Mbyte':1e6,'Gbyte':1e9,'nsecond':1e-3,'usecond':1,'msecond':1e3,'second':1e6}
 agg=collections.defaultdict(lambda: collections.defaultdict(float)); cnt=collections.Counter()
 for (i,name),m in per.items():
     if 'pty' not in name: continue
