@@ -284,8 +284,6 @@ def sweep_batched(state: ReconState, dataset, config: SolverConfig, group=None) 
         import torch.distributed as dist
         world, rank = dist.get_world_size(group), dist.get_rank(group)
     engaged = _engaged(st, config)
-    if engaged and world > 1:
-        raise ParameterError("position refinement with a multi-rank batched sweep is not supported yet")
     sense = _native.SENSE_NONE
     if engaged:
         sense = _native.SENSE_XCORR_A if config.posref.sensor == "XCORR_A" else _native.SENSE_XCORR_B
@@ -334,11 +332,12 @@ def sweep_batched(state: ReconState, dataset, config: SolverConfig, group=None) 
         args = _native.PtyBatchArgs(
             dcode, w, m, n, _native.ptr(st.obj), h, wc, st.canvas_origin[0], st.canvas_origin[1],
             _native.ptr(st.probe_stack), _native.ptr(pats), _native.ptr(pats_t), _native.ptr(st.positions),
-            _native.ptr(order_d) + 4 * (s + lo), max(hi - lo, 1), s + min(lo, nb - 1),
+            _native.ptr(order_d) + 4 * (s + min(lo, nb - 1)), max(hi - lo, 1), s + min(lo, nb - 1),
             float(config.alpha_obj), float(config.alpha_probe), float(config.beta),
             float(config.gamma), float(config.epsilon_rel), upd_probe,
-            int(bool(config.track_modulus_error)), sense, _native.ptr(stage),
-            _native.ptr(obj_acc), _native.ptr(probe_acc), _native.ptr(err_part),
+            int(bool(config.track_modulus_error)),
+            sense if hi > lo else _native.SENSE_NONE,        # stage o'_j only for this rank's positions
+            _native.ptr(stage), _native.ptr(obj_acc), _native.ptr(probe_acc), _native.ptr(err_part),
             _native.ptr(status), _native.ptr(ws), ws.numel())
         _native.batch_apply(args)
     if world > 1:
@@ -346,8 +345,25 @@ def sweep_batched(state: ReconState, dataset, config: SolverConfig, group=None) 
         dist.all_reduce(err_part, group=group)
         dist.all_reduce(status, op=dist.ReduceOp.MAX, group=group)
     _native.batch_finalize(err_part, n, w, err)
-    if engaged:
+    if engaged and world == 1:
         _refine_positions(st, config.posref, n, w)
+    elif engaged:
+        # every rank staged (o_j, o'_j) for its own slice of each batch; it
+        # senses and Adam-steps exactly those positions, then the disjoint
+        # updates are merged with a masked sum (x + 0 is exact) so positions
+        # and Adam state stay identical on every rank
+        mine = np.concatenate([order[s + batch_slice(min(b, n - s), rank, world)[0]:
+                                     s + batch_slice(min(b, n - s), rank, world)[1]]
+                               for s in range(0, n, b)]).astype(np.int32)
+        _refine_positions(st, config.posref, n, w, index=mine)
+        import torch.distributed as dist
+        mask = t.zeros((n,), dtype=t.bool, device=st.positions.device)
+        mask[t.from_numpy(mine).to(mask.device, t.int64)] = True
+        ad = st.adam
+        for buf in (st.positions, ad.m, ad.v, ad.t):
+            part = t.where(mask.view(-1, *([1] * (buf.dim() - 1))), buf, t.zeros_like(buf))
+            dist.all_reduce(part, group=group)
+            buf.copy_(part)
     if (config.ortho_interval > 0 and m > 1 and (st.iteration + 1) % config.ortho_interval == 0):
         _native.orthogonalize(st.probe_stack)
     he = st.buffer("err", (3,), t.float64, pinned=True)
@@ -454,12 +470,18 @@ def sweep_replicas(states, datasets, config: SolverConfig, orders=None, kernel_e
     return states
 
 
-def _refine_positions(st: ReconState, pc: PosRefConfig, n: int, w: int) -> None:
+def _refine_positions(st: ReconState, pc: PosRefConfig, n: int, w: int, index=None) -> None:
     """posref.py:57-113 for every position of the sweep, batched: register the
     staged pairs (XCORR_A: o_j vs o'_j; XCORR_B: modelled vs measured
-    intensity) with raw weighting, then the float64 Adam step + clamp."""
+    intensity) with raw weighting, then the float64 Adam step + clamp.
+    ``index`` (int32 numpy, optional): only these positions were staged."""
     t = _native.torch()
     stage = st.buffer("stage", (n, 2, w, w), st.obj.dtype)
+    idx_d = None
+    if index is not None:
+        idx_d = t.from_numpy(np.ascontiguousarray(index, np.int32)).to(stage.device)
+        stage = stage.index_select(0, idx_d.long())
+        n = int(idx_d.numel())
     dy = st.buffer("reg_dy", (n,), t.float64)
     dx = st.buffer("reg_dx", (n,), t.float64)
     peak = st.buffer("reg_peak", (n,), t.float64)
@@ -478,7 +500,7 @@ def _refine_positions(st: ReconState, pc: PosRefConfig, n: int, w: int) -> None:
             _native.register_batch(work[:e - s], w, e - s, 1, int(pc.kappa),
                                    dy[s:e], dx[s:e], peak[s:e], ok[s:e])
     # sensors return (gx, gy) = (est.dx, est.dy) (posref.py:63)
-    _native.adam_apply(st.positions, st.adam, dx, dy, ok, pc, position_bounds(st, w))
+    _native.adam_apply(st.positions, st.adam, dx, dy, ok, pc, position_bounds(st, w), index=idx_d)
 
 
 def run(dataset, config: SolverConfig, state: ReconState | None = None,
