@@ -250,7 +250,8 @@ struct UpdateParams {
 // shared accumulators (owner-only access).  Returns the team's max of the next
 // visit's sum_m |P_m|^2 (engine.py:129-132).  stg (XCORR_A planes) may be null.
 template <typename T, int W>
-__device__ __forceinline__ T task_row_inv_update(const cplx<T>* tw, cplx<T>* lines, cplx<T>* numer, T* pp, T* nppacc,
+__device__ __forceinline__ T task_row_inv_update(const cplx<T>* tw, cplx<T>* lines, cplx<T>* __restrict__ numer,
+                                                 T* __restrict__ pp, T* __restrict__ nppacc,
                                                  T* red4,
                                                  int team, int tl, int gi, int b, unsigned gmask, const cplx<T>* pos,
                                                  int M, int rq, cplx<T>* obj, int Wc, int ar, int ac, cplx<T>* probes,
@@ -279,11 +280,24 @@ __device__ __forceinline__ T task_row_inv_update(const cplx<T>* tw, cplx<T>* lin
     const T dmax_p = beta * omax + (T(1) - beta) * omax;
     for (int m = 0; m < M; ++m) {
         team_sync<TEAM>(team);
-        team_load_rows<T, W>(lines, pos + m * WW, rq, tl);
+        // scratch rows and probe row in flight together (one L2 round trip)
+        constexpr int NE = 4 * W / TEAM;
+        const C* src = pos + m * WW + 4 * rq;
+        C sv[NE];
+#pragma unroll
+        for (int i = 0; i < NE; ++i) {
+            const int e = tl + i * TEAM;
+            sv[i] = src[(size_t)(e >> 2) * W + (e & 3)];
+        }
         C* pr = probes + m * WW + (size_t)r * W;
         C pv[A];
 #pragma unroll
         for (int q = 0; q < A; ++q) pv[q] = pr[slot_col<W>(b, q)];
+#pragma unroll
+        for (int i = 0; i < NE; ++i) {
+            const int e = tl + i * TEAM;
+            lines[(e & 3) * LS4 + pad<W>(e >> 2)] = sv[i];
+        }
         team_sync<TEAM>(team);
         group_fft<T, W, true>(
             myline, tw, b, gmask, [&](int n, int) { return myline[pad<W>(n)]; },
