@@ -111,7 +111,9 @@ class ReconState:
     @probes.setter
     def probes(self, value):
         t = _native.torch()
-        stack = t.stack([v.to(self.obj.device, self.obj.dtype) for v in value])
+        # numpy arrays (the reference's type, engine.py:219-223) or tensors
+        stack = t.stack([(v if isinstance(v, t.Tensor) else t.as_tensor(np.asarray(v)))
+                         .to(self.obj.device, self.obj.dtype) for v in value])
         if self.frame_chirp is not None:
             stack = stack * self.frame_chirp
         self.probe_stack = stack.contiguous()

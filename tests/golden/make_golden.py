@@ -250,16 +250,45 @@ def gen_simulate(tmp):
     np.savez_compressed(OUT / "simulate.npz", **out)
 
 
+def gen_metrics(tmp):
+    """metrics.py:20-64 on a reconstructed scene (object error on the coverage
+    mask, position RMSE after the gauge shift)."""
+    sys.path.insert(0, str(REF))
+    import ptychokit.metrics as metrics
+    out = {}
+    g, plan, obj, probes, ds = scene(32, (4, 4), 7.0, 8.0, 2, (0.7, 0.3), 1.0, 5)
+    cfg = engine.SolverConfig(alpha_obj=0.9, alpha_probe=0.9, beta=0.5, gamma=0.5, mode_count=2)
+    st = engine.initialize(ds, cfg)
+    for _ in range(3):
+        engine.sweep(st, ds, cfg)
+    r0, c0 = st.canvas_origin
+    h, w = st.obj.shape
+    truth = obj[r0:r0 + h, c0:c0 + w]
+    out["recon"], out["truth"] = st.obj, truth
+    out["probes"], out["positions"] = np.stack(st.probes), st.positions
+    out["canvas_origin"] = np.array(st.canvas_origin)
+    for thr in (0.05, 0.3):
+        mask = metrics.coverage_mask(st.probes, st.positions, st.obj.shape, st.canvas_origin, thr)
+        out[f"mask_{thr}"] = mask
+        out[f"object_error_{thr}"] = np.array([metrics.object_error(st.obj, truth, mask)])
+    est = plan.true_positions + np.random.default_rng(9).normal(0, 0.3, plan.true_positions.shape) + 2.5
+    out["est"], out["true"] = est, plan.true_positions
+    out["position_rmse"] = np.array([metrics.position_rmse(est, plan.true_positions)])
+    np.savez_compressed(OUT / "metrics.npz", **out)
+
+
+GENERATORS = {"fields": lambda t: gen_fields(), "visit": gen_visit, "sweeps": gen_sweeps,
+              "registration": lambda t: gen_registration(), "adam": lambda t: gen_adam(),
+              "simulate": gen_simulate, "metrics": gen_metrics}
+
+
 def main():
     import tempfile
+    only = sys.argv[1:] or list(GENERATORS)
     with tempfile.TemporaryDirectory() as d:
         tmp = Path(d)
-        gen_fields()
-        gen_visit(tmp)
-        gen_sweeps(tmp)
-        gen_registration()
-        gen_adam()
-        gen_simulate(tmp)
+        for name in only:
+            GENERATORS[name](tmp)
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)
 
