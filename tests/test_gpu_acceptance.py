@@ -72,3 +72,114 @@ def test_criterion_6_position_refinement(gpu):
     assert rmse_a <= 0.30 * initial_rmse, (rmse_a, initial_rmse)
     assert objerr_a <= 0.5 * objerr_off, (objerr_a, objerr_off)
     assert rmse_b > rmse_a
+
+
+def _fft_c(a):
+    return np.fft.fftshift(np.fft.fft2(np.fft.ifftshift(a), norm="ortho"))
+
+
+def _ifft_c(a):
+    return np.fft.fftshift(np.fft.ifft2(np.fft.ifftshift(a), norm="ortho"))
+
+
+def _independent_mepie_sweep(obj, probes, positions, origin, patterns, alpha_o, alpha_p, eps_rel=1e-12):
+    """A straight-line multi-mode ePIE sweep with no package internals (the
+    reference test's own independent statement, test_acceptance.py:54-85)."""
+    w = probes[0].shape[0]
+    r0, c0 = origin
+    for j in range(len(positions)):
+        x, y = positions[j]
+        r = int(round(float(y))) - r0
+        c = int(round(float(x))) - c0
+        o_j = obj[r:r + w, c:c + w].copy()
+        psi_det = [_fft_c(p * o_j) for p in probes]
+        total = sum(np.abs(pd) ** 2 for pd in psi_det)
+        eps = eps_rel * max(total.max(), np.finfo(float).tiny)
+        corrected = [_ifft_c(np.sqrt(patterns[j]) * pd / np.sqrt(total + eps)) for pd in psi_det]
+        probe_power = sum(np.abs(p) ** 2 for p in probes)
+        denom_o = probe_power.max() * (1.0 + eps_rel)
+        new_o = o_j + alpha_o * sum((cp - p * o_j) * np.conj(p) for p, cp in zip(probes, corrected)) / denom_o
+        denom_p = (np.abs(o_j) ** 2).max() * (1.0 + eps_rel)
+        probes = [p + alpha_p * (cp - p * o_j) * np.conj(o_j) / denom_p for p, cp in zip(probes, corrected)]
+        obj[r:r + w, c:c + w] = new_o
+    return obj, probes
+
+
+def test_criterion_1_epie_reduction(gpu):
+    """beta = gamma = 1 is multi-mode ePIE (test_acceptance.py:88-118), fp64,
+    the reference's own 1e-12 bound over 50 iterations (measured 5.9e-14)."""
+    plan = pk.make_scan((7, 7), 10.0, 1.0, seed=2)
+    obj = pk.make_object(pk.canvas_shape_for(plan, 64), "spokes", seed=2)
+    probes = pk.make_probe(pk.ProbeSpec(2, (0.85, 0.15), "disk", 14.0), GEOM64)
+    ds = pk.synthesize(obj, probes, plan, GEOM64, noise="none", seed=2)
+    cfg = pk.SolverConfig(alpha_obj=0.9, alpha_probe=0.8, beta=1.0, gamma=1.0, mode_count=2,
+                          position_order="fixed", precision="fp64")
+    state = pk.initialize(ds, cfg)
+    ref_obj = state.obj.cpu().numpy().copy()
+    ref_probes = [p.cpu().numpy().copy() for p in state.probes]
+    worst = 0.0
+    for _ in range(50):
+        pk.sweep(state, ds, cfg)
+        ref_obj, ref_probes = _independent_mepie_sweep(ref_obj, ref_probes, ds.positions,
+                                                       state.canvas_origin, ds.patterns, 0.9, 0.8)
+        worst = max(worst, float(np.abs(state.obj.cpu().numpy() - ref_obj).max() / np.abs(ref_obj).max()))
+        for a, b in zip(state.probes, ref_probes):
+            worst = max(worst, float(np.abs(a.cpu().numpy() - b).max() / np.abs(b).max()))
+    assert worst <= 1e-12, worst
+
+
+def test_criterion_2_modulus_exactness(gpu):
+    """test_acceptance.py:121-139 (fp64: the modulus projection is exact to
+    round-off, the reference's 1e-9 bound)."""
+    plan = pk.make_scan((7, 7), 10.0, 1.0, seed=3)
+    obj = pk.make_object(pk.canvas_shape_for(plan, 64), "phase-screen", seed=3)
+    probes = pk.make_probe(pk.ProbeSpec(1, (1.0,), "disk", 14.0), GEOM64)
+    ds = pk.synthesize(obj, probes, plan, GEOM64, noise="none", seed=3)
+    cfg = pk.SolverConfig(iterations=100, track_modulus_error=True, precision="fp64")
+    state = pk.initialize(ds, cfg)
+    for _ in range(100):
+        pk.sweep(state, ds, cfg)
+    assert max(state.modulus_error_trace) <= 1e-9
+
+
+def _translation_aligned_object_error(state, dataset) -> float:
+    """test_acceptance.py:169-188 with this package's register/subpixel_shift."""
+    raw = recon_object_error(state, dataset)
+    mask = coverage_mask(state.probes, state.positions, tuple(state.obj.shape),
+                         state.canvas_origin).cpu().numpy()
+    r0, c0 = state.canvas_origin
+    h, w = state.obj.shape
+    truth = dataset.ground_truth.obj[r0:r0 + h, c0:c0 + w]
+    side = max(h, w)
+    a = np.zeros((side, side), complex)
+    b = np.zeros((side, side), complex)
+    o = state.obj.cpu().numpy().astype(np.complex128)
+    a[:h, :w] = np.where(mask, o, 0)
+    b[:h, :w] = np.where(mask, truth, 0)
+    if side & (side - 1):     # this package's FFT takes power-of-two windows
+        p2 = 1 << side.bit_length()
+        a = np.pad(a, ((0, p2 - side), (0, p2 - side)))
+        b = np.pad(b, ((0, p2 - side), (0, p2 - side)))
+    est = pk.register(b, a, weighting="raw", upsample=100)
+    # fields.py:110-122 on the (non power-of-two) canvas: host numpy, test side
+    fy = np.fft.fftfreq(h)[:, None]
+    fx = np.fft.fftfreq(w)[None, :]
+    shifted = np.fft.ifft2(np.fft.fft2(o) * np.exp(-2j * np.pi * (fy * est.dy + fx * est.dx)))
+    aligned = object_error(shifted, truth, mask)
+    return min(raw, aligned)
+
+
+def test_criterion_4_two_mode_recovery(gpu):
+    plan = pk.make_scan((7, 7), 9.0, 2.0, seed=4)
+    obj = pk.make_object(pk.canvas_shape_for(plan, 64), "spokes", seed=4)
+    probes = pk.make_probe(pk.ProbeSpec(2, (0.85, 0.15), "disk", 15.0), GEOM64)
+    ds = pk.synthesize(obj, probes, plan, GEOM64, noise="none", seed=4)
+    ds.positions[:] = ds.ground_truth.true_positions
+    errs = {}
+    for mode_count in (1, 2):
+        cfg = pk.SolverConfig(iterations=300, mode_count=mode_count, shuffle_seed=1)
+        state = pk.initialize(ds, cfg)
+        for _ in range(300):
+            pk.sweep(state, ds, cfg)
+        errs[mode_count] = _translation_aligned_object_error(state, ds)
+    assert errs[2] / errs[1] <= 0.5, errs
