@@ -53,6 +53,7 @@ struct SweepDev {
     void* peak_part;              // [2][nslots][W/4] real
     void* tmax_part;              // [nslots][W] real
     double* err_part;             // [nslots][N][W][3] per-visit, per-column error terms
+    void* ppg;                    // [nslots][W][W] real: sum_m |P_m|^2 of the current probes
     const void* twiddles;         // [W] complex, global
     unsigned long long* timeline; // debug: [steps][5][gridDim] globaltimer stamps or null
     int timeline_steps;
@@ -212,11 +213,13 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
     for (int item = cta; item < S * nq; item += ncta) {
         const int s = s0 + item / nq, rq = item % nq;
         const C* probes = reinterpret_cast<const C*>(P.slot[s].probes);
+        T* ppg = reinterpret_cast<T*>(P.ppg) + (size_t)s * WW;
         T pk = T(0);
         for (int i = tid; i < 4 * W; i += NT) {
             const size_t off = (size_t)(4 * rq) * W + i;
             T pp = T(0);
             for (int m = 0; m < M; ++m) pp += norm2(probes[m * WW + off]);
+            ppg[off] = pp;
             pk = fmax(pk, pp);
         }
         pk = block_max(pk, red);
@@ -313,6 +316,7 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
             C* stg = P.sense == PTY_SENSE_XCORR_A ? reinterpret_cast<C*>(sl.stage) + (size_t)j * 2 * WW : nullptr;
             const T npk = task_row_inv_update<T, W>(tw, lines, numer, ppacc, nppacc, red4_p4, team, tl, gi, b, gmask,
                                                     scratch + (size_t)s * M * WW, M, rq, reinterpret_cast<C*>(sl.obj),
+                                                    reinterpret_cast<T*>(P.ppg) + (size_t)s * WW,
                                                     sl.Wc, s_ar[s], s_ac[s], reinterpret_cast<C*>(sl.probes), peak,
                                                     omax, U, stg);
             if (tl == 0) peak_part[((size_t)((step + 1) & 1) * P.nslots + s) * nq + rq] = npk;

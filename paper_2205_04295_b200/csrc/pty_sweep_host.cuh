@@ -20,6 +20,7 @@ struct SweepLayout {
     void* tmax;
     double* err_part;
     double* visit_sum;
+    void* ppg;
     size_t bytes;
 };
 
@@ -36,6 +37,7 @@ inline SweepLayout carve_sweep(void* ws, int W, int M, int N, int S) {
     L.tmax = c.take<void>((size_t)S * W * sizeof(T));
     L.err_part = c.take<double>((size_t)S * N * W * 3 * sizeof(double));
     L.visit_sum = c.take<double>((size_t)S * N * 3 * sizeof(double));
+    L.ppg = c.take<void>((size_t)S * W * W * sizeof(T));
     L.bytes = c.off;
     return L;
 }
@@ -75,7 +77,7 @@ int run_sweep_lines(const PtySweepArgs* a, cudaStream_t st) {
     P.update_probe = a->update_probe; P.track_mod = a->track_modulus; P.sense = a->sense;
     P.barrier = L.barrier; P.anchors = L.anchors; P.scratch = L.scratch; P.totT = L.totT;
     P.omax_part = L.omax; P.peak_part = L.peak; P.tmax_part = L.tmax;
-    P.err_part = L.err_part; P.twiddles = tw;
+    P.err_part = L.err_part; P.twiddles = tw; P.ppg = L.ppg;
     ErrOut outs{};
     for (int s = 0; s < S; ++s) {
         const PtySlot& h = a->slots[s];

@@ -251,11 +251,12 @@ struct UpdateParams {
 // visit's sum_m |P_m|^2 (engine.py:129-132).  stg (XCORR_A planes) may be null.
 template <typename T, int W>
 __device__ __forceinline__ T task_row_inv_update(const cplx<T>* tw, cplx<T>* lines, cplx<T>* __restrict__ numer,
-                                                 T* __restrict__ pp, T* __restrict__ nppacc,
+                                                 T* __restrict__ invdp, T* __restrict__ nppacc,
                                                  T* red4,
                                                  int team, int tl, int gi, int b, unsigned gmask, const cplx<T>* pos,
-                                                 int M, int rq, cplx<T>* obj, int Wc, int ar, int ac, cplx<T>* probes,
-                                                 T peak, T omax, const UpdateParams& U, cplx<T>* stg) {
+                                                 int M, int rq, cplx<T>* obj, T* ppg, int Wc, int ar, int ac,
+                                                 cplx<T>* probes, T peak, T omax, const UpdateParams& U,
+                                                 cplx<T>* stg) {
     using C = cplx<T>;
     constexpr int A = Shape<W>::A, B = Shape<W>::B, TEAM = 4 * B, LS4 = team_line_stride<W>();
     const size_t WW = (size_t)W * W;
@@ -264,20 +265,26 @@ __device__ __forceinline__ T task_row_inv_update(const cplx<T>* tw, cplx<T>* lin
             eps_rel = T(U.eps_rel);
     const int r = 4 * rq + gi;
     C* orow = obj + (size_t)(ar + r) * Wc + ac;
+    T* pprow = ppg + (size_t)r * W;
     C* myline = lines + gi * LS4;
     C* nrow = numer + gi * W;
-    T* prow_pp = pp + gi * W;
+    T* idp = invdp + gi * W;
     T* npp = nppacc + gi * W;
+    const T dmax_p = beta * omax + (T(1) - beta) * omax;
     C ov[A];
+#pragma unroll
+    for (int q = 0; q < A; ++q) ov[q] = orow[slot_col<W>(b, q)];
 #pragma unroll
     for (int q = 0; q < A; ++q) {
         const int c = slot_col<W>(b, q);
-        ov[q] = orow[c];
         nrow[c] = C{T(0), T(0)};
-        prow_pp[c] = T(0);
         npp[c] = T(0);
+        // the probe-update denominator (engine.py:148-150) is mode-invariant:
+        // one reciprocal per element (divr multiplies by it, numpy's complex/real)
+        T dp = beta * omax + (T(1) - beta) * norm2(ov[q]);
+        dp = dp + eps_rel * dmax_p;
+        idp[c] = T(1) / dp;
     }
-    const T dmax_p = beta * omax + (T(1) - beta) * omax;
     for (int m = 0; m < M; ++m) {
         team_sync<TEAM>(team);
         // scratch rows and probe row in flight together (one L2 round trip)
@@ -305,25 +312,25 @@ __device__ __forceinline__ T task_row_inv_update(const cplx<T>* tw, cplx<T>* lin
                 const C o = ov[q];
                 const C d = scale(X, checker<T>(r, c) * invW2) - pv[q] * o;
                 nrow[c] = nrow[c] + mulc(d, pv[q]);
-                prow_pp[c] += norm2(pv[q]);
                 if (U.update_probe) {
-                    T no2 = norm2(o);
-                    opaque(no2);
-                    T dp = beta * omax + (T(1) - beta) * no2;
-                    dp = dp + eps_rel * dmax_p;
-                    const C np_ = pv[q] + divr(mulc(scale(d, alpha_p), o), dp);
+                    const C np_ = pv[q] + scale(mulc(scale(d, alpha_p), o), idp[c]);
                     pr[c] = np_;
                     npp[c] += norm2(np_);
                 }
             });
     }
+    // sum_m |P_m|^2 of this visit's probes: kept from the previous visit's
+    // update (same values, same mode order) or phase 0.  All loads first.
+    T ppv[A];
+#pragma unroll
+    for (int q = 0; q < A; ++q) ppv[q] = pprow[slot_col<W>(b, q)];
     const T dmax_o = gamma * peak + (T(1) - gamma) * peak;
     T pk = T(0);
 #pragma unroll
     for (int q = 0; q < A; ++q) {
         const int c = slot_col<W>(b, q);
         const C o = ov[q];
-        T den = gamma * peak + (T(1) - gamma) * prow_pp[c];
+        T den = gamma * peak + (T(1) - gamma) * ppv[q];
         den = den + eps_rel * dmax_o;
         const C no = o + divr(scale(nrow[c], alpha_o), den);
         orow[c] = o + (no - o);                                // paste_add_inplace
@@ -331,7 +338,13 @@ __device__ __forceinline__ T task_row_inv_update(const cplx<T>* tw, cplx<T>* lin
             stg[(size_t)r * W + c] = o;
             stg[WW + (size_t)r * W + c] = no;
         }
-        pk = fmax(pk, U.update_probe ? npp[c] : prow_pp[c]);
+        if (U.update_probe) {
+            const T nv = npp[c];
+            pprow[c] = nv;
+            pk = fmax(pk, nv);
+        } else {
+            pk = fmax(pk, ppv[q]);
+        }
     }
     return team_max4<W>(pk, red4, team, gi, b);
 }
