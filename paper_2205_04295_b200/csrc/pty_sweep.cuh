@@ -44,6 +44,7 @@ struct SweepDev {
     int W, M, N, nslots;
     double alpha_o, alpha_p, beta, gamma, eps_rel;
     int update_probe, track_mod, sense;
+    int resident;                 // P2 -> P3 column lines stay in shared memory (<= 1 column task per group)
     // workspace
     unsigned int* barrier;
     int* anchors;                 // [nslots][N][2]
@@ -180,6 +181,7 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
     T* tmax_part = reinterpret_cast<T*>(P.tmax_part);
     // phase-region views
     C* xch = reinterpret_cast<C*>(region) + grp * XS;                          // P1-P3
+    C* res = reinterpret_cast<C*>(region) + (size_t)grp * P.M * XS;            // P2-P3 resident lines
     C* tt = reinterpret_cast<C*>(region) + (size_t)NGRP * XS + (size_t)team * W * 5;   // P1
     T* red4_p1 = reinterpret_cast<T*>(reinterpret_cast<C*>(region) + (size_t)NGRP * XS + (size_t)NTEAM * W * 5) + team * 4;
     C* lines = reinterpret_cast<C*>(region) + (size_t)team * 4 * LS4;                  // P4
@@ -270,7 +272,8 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
         for (int task = cta * NGRP + grp; task < S * W; task += ncta * NGRP) {
             const int s = s0 + task / W, kc = task % W;
             if (s_dead[s]) continue;
-            const T tm = task_col_fwd<T, W>(tw, xch, b, gmask, scratch + (size_t)s * M * WW, M, kc, totT + (size_t)s * WW);
+            const T tm = task_col_fwd<T, W>(tw, xch, b, gmask, scratch + (size_t)s * M * WW, M, kc, totT + (size_t)s * WW,
+                                            P.resident ? res : nullptr);
             if (b == 0) tmax_part[(size_t)s * W + kc] = tm;
         }
         stamp(step, 2);
@@ -285,7 +288,7 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
             task_col_mod<T, W>(tw, xch, b, gmask, scratch + (size_t)s * M * WW, M, kc, totT + (size_t)s * WW,
                                tmax_part + (size_t)s * W, reinterpret_cast<const T*>(sl.patterns_t) + (size_t)j * WW,
                                T(P.eps_rel), P.track_mod, stg,
-                               P.err_part + (((size_t)s * N + step) * W + kc) * 3);
+                               P.err_part + (((size_t)s * N + step) * W + kc) * 3, P.resident ? res : nullptr);
         }
         stamp(step, 3);
         phase_sync();

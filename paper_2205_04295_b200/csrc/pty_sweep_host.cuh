@@ -95,7 +95,17 @@ int run_sweep_lines(const PtySweepArgs* a, cudaStream_t st) {
     // PTY_CTAS_PER_SM overrides downwards.  Cluster flavour (PTY_CLUSTER=K):
     // one cluster of K CTAs per slot, slots scheduled independently (measured
     // slower at 16 replicas: 8 clusters of 16 fit the GPCs at once).
-    const size_t smem = sweep_smem_fixed<T, W>() + sweep_smem_phase<T, W>(kSweepThreads);
+    // P2 -> P3 residency: every group owns at most one column task per step and
+    // its M transformed lines fit next to the phase region with 2 CTAs per SM
+    constexpr int NGRP = kSweepThreads / Shape<W>::B;
+    const size_t res_bytes = (size_t)NGRP * M * xch_size<W>() * sizeof(cplx<T>);
+    const size_t base_phase = sweep_smem_phase<T, W>(kSweepThreads);
+    const int want_res = env_int("PTY_RESIDENT", 1);
+    const size_t res_phase = std::max(base_phase, res_bytes);
+    const bool res_fit = 2 * (sweep_smem_fixed<T, W>() + res_phase + 1024) <= max_smem_per_sm();
+    const int grid_ctas = sm_count() * kSweepMaxCtasPerSm;
+    P.resident = (want_res && res_fit && (long)S * W <= (long)grid_ctas * NGRP && env_int("PTY_CLUSTER", 0) == 0) ? 1 : 0;
+    const size_t smem = sweep_smem_fixed<T, W>() + (P.resident ? res_phase : base_phase);
     if (smem > max_dyn_smem()) return PTY_ERR_ARGUMENT;
     int K = std::max(0, env_int("PTY_CLUSTER", 0));
     int grid = 0;
@@ -136,6 +146,7 @@ int run_sweep_lines(const PtySweepArgs* a, cudaStream_t st) {
         const int want = env_int("PTY_CTAS_PER_SM", 0);
         if (want > 0) per_sm = std::min(per_sm, want);
         grid = sm_count() * per_sm;
+        if ((long)S * W > (long)grid * NGRP) P.resident = 0;   // more than one column task per group
     }
 
     // debug timeline (PTY_TIMELINE=<steps>): per-CTA phase completion stamps

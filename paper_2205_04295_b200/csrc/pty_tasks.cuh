@@ -122,7 +122,7 @@ __device__ __forceinline__ T task_row_fwd(const cplx<T>* tw, cplx<T>* xch, cplx<
 // 114-116) stored transposed; returns the column's max(total).
 template <typename T, int W>
 __device__ __forceinline__ T task_col_fwd(const cplx<T>* tw, cplx<T>* xch, int b, unsigned gmask, cplx<T>* pos, int M,
-                                          int kc, T* totT_pos) {
+                                          int kc, T* totT_pos, cplx<T>* res = nullptr) {
     using C = cplx<T>;
     constexpr int A = Shape<W>::A, B = Shape<W>::B;
     const size_t WW = (size_t)W * W;
@@ -130,14 +130,24 @@ __device__ __forceinline__ T task_col_fwd(const cplx<T>* tw, cplx<T>* xch, int b
     T tot[A];
 #pragma unroll
     for (int q = 0; q < A; ++q) tot[q] = T(0);
-    for (int m = 0; m < M; ++m) {
+    for (int m = 0; m < M;++m) {
         C* line = pos + m * WW + (size_t)kc * W;
-        group_fft<T, W, false>(
-            xch, tw, b, gmask, [&](int n, int) { return line[n]; },
-            [&](int u, int slot, C v) {
-                line[u] = v;
-                tot[slot] += norm2(v) * invW2;
-            });
+        if (res) {   // Psi_m stays in this group's shared-memory line for P3
+            C* rl = res + m * xch_size<W>();
+            group_fft<T, W, false>(
+                rl, tw, b, gmask, [&](int n, int) { return line[n]; },
+                [&](int u, int slot, C v) {
+                    rl[pad<W>(u)] = v;
+                    tot[slot] += norm2(v) * invW2;
+                });
+        } else {
+            group_fft<T, W, false>(
+                xch, tw, b, gmask, [&](int n, int) { return line[n]; },
+                [&](int u, int slot, C v) {
+                    line[u] = v;
+                    tot[slot] += norm2(v) * invW2;
+                });
+        }
     }
     T tm = T(0);
     T* trow = totT_pos + (size_t)kc * W;
@@ -158,7 +168,8 @@ __device__ __forceinline__ T task_col_fwd(const cplx<T>* tw, cplx<T>* xch, int b
 template <typename T, int W>
 __device__ __forceinline__ void task_col_mod(const cplx<T>* tw, cplx<T>* xch, int b, unsigned gmask, cplx<T>* pos,
                                              int M, int kc, const T* totT_pos, const T* tmax_pos, const T* It_pos,
-                                             T eps_rel, int track, cplx<T>* stg, double* err) {
+                                             T eps_rel, int track, cplx<T>* stg, double* err,
+                                             cplx<T>* res = nullptr) {
     using C = cplx<T>;
     constexpr int A = Shape<W>::A, B = Shape<W>::B;
     const size_t WW = (size_t)W * W;
@@ -189,10 +200,11 @@ __device__ __forceinline__ void task_col_mod(const cplx<T>* tw, cplx<T>* xch, in
     }
     for (int m = 0; m < M; ++m) {
         C* line = pos + m * WW + (size_t)kc * W;
+        C* rl = res ? res + m * xch_size<W>() : nullptr;   // resident Psi_m from P2
         group_fft<T, W, true>(
-            xch, tw, b, gmask,
+            rl ? rl : xch, tw, b, gmask,
             [&](int n, int a) {
-                const C v = scale(line[n], sc[a]);
+                const C v = scale(rl ? rl[pad<W>(n)] : line[n], sc[a]);
                 after[a] += norm2(v) * invW2;
                 return v;
             },
