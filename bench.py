@@ -269,6 +269,69 @@ def e2e_arm(args, states, ds, cfg, dev, world):
             "d2h_bytes_per_step": int(d2h)}
 
 
+# ------------------------------------------- other named configs (1, 3, 4) ----
+CONFIGS = {
+    # BASELINE.json configs[0], [2], [3]
+    "config1": dict(W=128, M=1, grid=(10, 10), step=16.0, radius=30.0, powers=(1.0,), lam=8.3187e-10,
+                    posref=False, propagator="farfield"),
+    "config3": dict(W=256, M=3, grid=(20, 20), step=32.0, radius=60.0, powers=(0.8, 0.1, 0.1), lam=8.3187e-10,
+                    posref=True, propagator="farfield"),
+    "config4": dict(W=512, M=5, grid=(40, 40), step=64.0, radius=120.0, powers=(0.8, 0.05, 0.05, 0.05, 0.05),
+                    lam=8.29e-10, posref=True, propagator="fresnel"),
+}
+
+
+def configs_leg(args):
+    """Single-reconstruction throughput (exact reference order) of the other
+    named shapes: positions/s, iterations/s and the algorithmic-bytes
+    roofline fraction.  Config 3/4: +-2 px injected position errors, posref
+    XCORR_A kappa=10 engaged from the first sweep; config 4 with the Fresnel
+    propagator (extension)."""
+    import torch
+    import paper_2205_04295_b200 as pk
+    hbm, _ = peaks()
+    out = {}
+    for name, c in CONFIGS.items():
+        try:
+            w, m = c["W"], c["M"]
+            geom = pk.Geometry.create(c["lam"], 0.75, 20e-6, w)
+            plan = pk.make_scan(c["grid"], c["step"], 1.0, seed=1)
+            obj = pk.make_object(pk.canvas_shape_for(plan, w), "spokes", seed=1)
+            probes = pk.make_probe(pk.ProbeSpec(m, c["powers"], "disk", c["radius"]), geom)
+            ds = pk.synthesize(obj, probes, plan, geom, noise="none", seed=1, propagator=c["propagator"])
+            ds.patterns = ds.patterns.astype(np.float32)
+            if c["posref"]:
+                ds.positions = ds.positions + np.random.default_rng(42).uniform(-2, 2, ds.positions.shape)
+            posref = pk.PosRefConfig(sensor="XCORR_A", kappa=10, warmup_iterations=0) if c["posref"] else None
+            cfg = pk.SolverConfig(alpha_obj=0.9, alpha_probe=0.9, beta=0.5, gamma=0.5, mode_count=m,
+                                  position_order="shuffled", shuffle_seed=0, precision=args.precision,
+                                  posref=posref, propagator=c["propagator"])
+            st = pk.initialize(ds, cfg)
+            for _ in range(2):
+                pk.sweep(st, ds, cfg)
+            steps = 3 if w >= 512 else 5
+            torch.cuda.synchronize()
+            a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(steps):
+                pk.sweep(st, ds, cfg)
+            e.record()
+            torch.cuda.synchronize()
+            ms = a.elapsed_time(e) / steps
+            n = ds.n_positions
+            bpos = w * w * (20 + 16 * m)
+            out[name] = {"window": w, "modes": m, "positions": n, "posref": c["posref"],
+                         "propagator": c["propagator"], "positions_per_s": n / (ms / 1e3),
+                         "iterations_per_s": 1e3 / ms, "ms_per_iteration": ms,
+                         "roofline_frac": n / (ms / 1e3) * bpos / (hbm * 1e9),
+                         "error_trace_last": st.error_trace[-1]}
+        except Exception as exc:                      # report, never lose the main line
+            out[name] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        finally:
+            torch.cuda.empty_cache()
+    return out
+
+
 # ----------------------------------------------- batched leg (config 5) ----
 def batched_leg(args, rank, world):
     """BASELINE configs[4]: batched semi-parallel rPIE, 6400 positions of
@@ -421,6 +484,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-single", action="store_true")
     ap.add_argument("--no-batched", action="store_true")
+    ap.add_argument("--no-configs", action="store_true")
     ap.add_argument("--batch", type=int, default=1600)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
@@ -463,6 +527,9 @@ def main():
             batched = batched_leg(args, rank, world)
         except Exception as exc:                      # report, never lose the main line
             batched = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+    configs = None
+    if rank == 0 and not args.no_configs:
+        configs = configs_leg(args)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         vals = cpu_reference(workers, args.cpu_sample, 1)
@@ -491,6 +558,7 @@ def main():
             "clocks": res["clocks"],
             "single_reconstruction": res["single"],
             "batched": batched,
+            "configs": configs,
             "iterations_per_s": 1e3 / res["ms_per_step"],
         }
         print(json.dumps(line), flush=True)
