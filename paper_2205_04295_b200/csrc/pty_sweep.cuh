@@ -272,8 +272,9 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
         for (int task = cta * NGRP + grp; task < S * W; task += ncta * NGRP) {
             const int s = s0 + task / W, kc = task % W;
             if (s_dead[s]) continue;
-            const T tm = task_col_fwd<T, W>(tw, xch, b, gmask, scratch + (size_t)s * M * WW, M, kc, totT + (size_t)s * WW,
-                                            P.resident ? res : nullptr);
+            const T tm = P.resident
+                ? task_col_fwd<T, W, true>(tw, xch, b, gmask, scratch + (size_t)s * M * WW, M, kc, totT + (size_t)s * WW, res)
+                : task_col_fwd<T, W, false>(tw, xch, b, gmask, scratch + (size_t)s * M * WW, M, kc, totT + (size_t)s * WW);
             if (b == 0) tmax_part[(size_t)s * W + kc] = tm;
         }
         stamp(step, 2);
@@ -285,10 +286,14 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
             const SlotDev& sl = P.slot[s];
             const int j = s_j[s];
             C* stg = P.sense == PTY_SENSE_XCORR_B ? reinterpret_cast<C*>(sl.stage) + (size_t)j * 2 * WW : nullptr;
-            task_col_mod<T, W>(tw, xch, b, gmask, scratch + (size_t)s * M * WW, M, kc, totT + (size_t)s * WW,
-                               tmax_part + (size_t)s * W, reinterpret_cast<const T*>(sl.patterns_t) + (size_t)j * WW,
-                               T(P.eps_rel), P.track_mod, stg,
-                               P.err_part + (((size_t)s * N + step) * W + kc) * 3, P.resident ? res : nullptr);
+            const T* It = reinterpret_cast<const T*>(sl.patterns_t) + (size_t)j * WW;
+            double* ep = P.err_part + (((size_t)s * N + step) * W + kc) * 3;
+            if (P.resident)
+                task_col_mod<T, W, true>(tw, xch, b, gmask, scratch + (size_t)s * M * WW, M, kc, totT + (size_t)s * WW,
+                                         tmax_part + (size_t)s * W, It, T(P.eps_rel), P.track_mod, stg, ep, res);
+            else
+                task_col_mod<T, W, false>(tw, xch, b, gmask, scratch + (size_t)s * M * WW, M, kc, totT + (size_t)s * WW,
+                                          tmax_part + (size_t)s * W, It, T(P.eps_rel), P.track_mod, stg, ep);
         }
         stamp(step, 3);
         phase_sync();

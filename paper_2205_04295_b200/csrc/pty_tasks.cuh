@@ -120,7 +120,7 @@ __device__ __forceinline__ T task_row_fwd(const cplx<T>* tw, cplx<T>* xch, cplx<
 // Column pass, group task (column kc) of one position: forward column DFTs of
 // every mode written back in place (Psi), total = sum_m |Psi_m|^2 (engine.py:
 // 114-116) stored transposed; returns the column's max(total).
-template <typename T, int W>
+template <typename T, int W, bool RES = false>
 __device__ __forceinline__ T task_col_fwd(const cplx<T>* tw, cplx<T>* xch, int b, unsigned gmask, cplx<T>* pos, int M,
                                           int kc, T* totT_pos, cplx<T>* res = nullptr) {
     using C = cplx<T>;
@@ -132,7 +132,7 @@ __device__ __forceinline__ T task_col_fwd(const cplx<T>* tw, cplx<T>* xch, int b
     for (int q = 0; q < A; ++q) tot[q] = T(0);
     for (int m = 0; m < M;++m) {
         C* line = pos + m * WW + (size_t)kc * W;
-        if (res) {   // Psi_m stays in this group's shared-memory line for P3
+        if constexpr (RES) {   // Psi_m stays in this group's shared-memory line for P3
             C* rl = res + m * xch_size<W>();
             group_fft<T, W, false>(
                 rl, tw, b, gmask, [&](int n, int) { return line[n]; },
@@ -165,7 +165,7 @@ __device__ __forceinline__ T task_col_fwd(const cplx<T>* tw, cplx<T>* xch, int b
 // tmax_pos: the position's W column maxima; It: the transposed pattern.
 // stg (XCORR_B sensor planes, row-major total and I) may be null.
 // Writes err[0..2] = (sum (sqrt(total)-sqrt(I))^2, sum I, worst modulus error).
-template <typename T, int W>
+template <typename T, int W, bool RES = false>
 __device__ __forceinline__ void task_col_mod(const cplx<T>* tw, cplx<T>* xch, int b, unsigned gmask, cplx<T>* pos,
                                              int M, int kc, const T* totT_pos, const T* tmax_pos, const T* It_pos,
                                              T eps_rel, int track, cplx<T>* stg, double* err,
@@ -200,11 +200,11 @@ __device__ __forceinline__ void task_col_mod(const cplx<T>* tw, cplx<T>* xch, in
     }
     for (int m = 0; m < M; ++m) {
         C* line = pos + m * WW + (size_t)kc * W;
-        C* rl = res ? res + m * xch_size<W>() : nullptr;   // resident Psi_m from P2
+        C* rl = RES ? res + m * xch_size<W>() : xch;      // resident Psi_m from P2
         group_fft<T, W, true>(
-            rl ? rl : xch, tw, b, gmask,
+            rl, tw, b, gmask,
             [&](int n, int a) {
-                const C v = scale(rl ? rl[pad<W>(n)] : line[n], sc[a]);
+                const C v = scale(RES ? rl[pad<W>(n)] : line[n], sc[a]);
                 after[a] += norm2(v) * invW2;
                 return v;
             },
