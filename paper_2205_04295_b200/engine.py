@@ -395,7 +395,13 @@ def sweep_replicas(states, datasets, config: SolverConfig, orders=None, kernel_e
     if len(states) != len(datasets) or not states:
         raise ParameterError("need one dataset per state")
     if len(states) > _native.MAX_SLOTS:
-        raise ParameterError(f"at most {_native.MAX_SLOTS} replicas per launch")
+        # more replicas than one launch carries: consecutive launches of at
+        # most MAX_SLOTS (each replica's sweep is still one launch)
+        for lo in range(0, len(states), _native.MAX_SLOTS):
+            hi = lo + _native.MAX_SLOTS
+            sweep_replicas(states[lo:hi], datasets[lo:hi], config,
+                           None if orders is None else orders[lo:hi], kernel_events)
+        return states
     t0 = time.perf_counter()
     s0 = states[0]
     w, m = s0.window, int(s0.probe_stack.shape[0])
