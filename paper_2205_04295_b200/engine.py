@@ -310,6 +310,11 @@ def sweep_batched(state: ReconState, dataset, config: SolverConfig, group=None) 
     order_d.copy_(order_h, non_blocking=True)
     ws = _native.workspace(_native.batch_workspace_bytes(dcode, w, m, b, h, wc), "batch")
     upd_probe = int(bool(config.update_probe_modes) and config.alpha_probe > 0)
+    if world > 1:
+        # canvas rows a batch can touch (union over ALL its positions, so the
+        # band is identical on every rank): only that band of the object
+        # accumulator is all-reduced -- the rest is zero on every rank
+        rows_h = np.rint(st.positions[:, 1].cpu().numpy()).astype(np.int64) - st.canvas_origin[0]
     for s in range(0, n, b):
         nb = min(b, n - s)
         lo, hi = batch_slice(nb, rank, world)
@@ -329,7 +334,10 @@ def sweep_batched(state: ReconState, dataset, config: SolverConfig, group=None) 
             probe_acc.zero_()
         if world > 1:
             import torch.distributed as dist
-            dist.all_reduce(obj_acc, group=group)
+            rb = rows_h[order[s:s + nb]]
+            r_lo, r_hi = max(0, int(rb.min())), min(h, int(rb.max()) + w)
+            for plane in range(3):
+                dist.all_reduce(obj_acc[plane, r_lo:r_hi], group=group)
             dist.all_reduce(probe_acc, group=group)
         args = _native.PtyBatchArgs(
             dcode, w, m, n, _native.ptr(st.obj), h, wc, st.canvas_origin[0], st.canvas_origin[1],
