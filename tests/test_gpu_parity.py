@@ -450,3 +450,33 @@ def test_line_task_kernels_match_tile_kernel(gpu, monkeypatch, env):
     assert rel_l2(b.obj.cpu().numpy(), a.obj.cpu().numpy()) < 1e-12
     assert rel_l2(b.probe_stack.cpu().numpy(), a.probe_stack.cpu().numpy()) < 1e-12
     np.testing.assert_allclose(b.error_trace, a.error_trace, rtol=1e-12)
+
+
+@pytest.mark.parametrize("w,m,posref,replicas", [(16, 1, False, 1), (32, 8, True, 1), (64, 4, False, 9),
+                                                 (128, 2, True, 12), (32, 3, False, 24)])
+def test_shape_sweep_vs_oracle(gpu, w, m, posref, replicas):
+    """Every window / mode-count corner (W 16..128, M 1..8) and every kernel
+    flavour (tiles for <= 8 slots, line tasks with resident columns above),
+    fp64 against the oracle for 2 sweeps; every replica equals its own oracle."""
+    geom = pk.Geometry.create(8.3187e-10, 0.75, 20e-6, w)
+    plan = pk.make_scan((3, 3), w / 4, 1.0, seed=w + m)
+    obj = pk.make_object(pk.canvas_shape_for(plan, w), "spokes", seed=w)
+    powers = (1.0,) if m == 1 else tuple([0.6] + [0.4 / (m - 1)] * (m - 1))
+    probes = pk.make_probe(pk.ProbeSpec(m, powers, "disk", w * 0.3), geom)
+    ds = pk.synthesize(obj, probes, plan, geom)
+    ds.patterns = ds.patterns.astype(np.float32).astype(np.float64)
+    ds.positions = ds.positions + np.random.default_rng(1).uniform(-1, 1, ds.positions.shape)
+    cfg = pk.SolverConfig(alpha_obj=0.9, alpha_probe=0.9, beta=0.5, gamma=0.5, mode_count=m, precision="fp64",
+                          posref=pk.PosRefConfig(kappa=10, warmup_iterations=0) if posref else None)
+    states = [pk.initialize(ds, pk.SolverConfig(**{**cfg.__dict__, "init_seed": r})) for r in range(replicas)]
+    oracles = [rpie.initialize(ds.patterns, ds.positions, w, pk.SolverConfig(**{**cfg.__dict__, "init_seed": r}))
+               for r in range(replicas)]
+    for _ in range(2):
+        pk.sweep_replicas(states, [ds] * replicas, cfg)
+        for o in oracles:
+            rpie.sweep(o, ds.patterns, w, cfg)
+    for st, o in zip(states, oracles):
+        assert rel_l2(st.obj.cpu().numpy(), o.obj) < 1e-10
+        assert rel_l2(st.probe_stack.cpu().numpy(), np.stack(o.probes)) < 1e-10
+        np.testing.assert_allclose(st.positions.cpu().numpy(), o.positions, rtol=0, atol=1e-9)
+        np.testing.assert_allclose(st.error_trace, o.error_trace, rtol=1e-10)
