@@ -156,10 +156,11 @@ _ws = {}
 
 
 def workspace(nbytes: int, tag: str = "sweep"):
-    """A cached uint8 device buffer of at least ``nbytes`` (per device, per tag)."""
+    """A cached uint8 device buffer of at least ``nbytes`` (per device, per
+    stream, per tag: calls on different streams never share scratch)."""
     t = torch()
     dev = device()
-    key = (dev.index, tag)
+    key = (dev.index, t.cuda.current_stream(dev).cuda_stream, tag)
     buf = _ws.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = t.empty(max(int(nbytes), 1), dtype=t.uint8, device=dev)

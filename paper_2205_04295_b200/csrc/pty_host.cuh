@@ -8,6 +8,7 @@
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <type_traits>
 #include <vector>
 
@@ -90,15 +91,24 @@ inline size_t max_dyn_smem() {
 }
 
 // ------------------------------------------------------------- twiddles --
-// Twiddle tables live in one static device buffer per (dtype, W), built once.
+// Twiddle tables: one device buffer per (device, dtype, W), built once on
+// first use (float64 twiddle_kernel, then rounded); guarded for callers on
+// several host threads / devices.
+constexpr int kMaxDevices = 64;
 template <typename T, int W> inline const cplx<T>* twiddles(cudaStream_t st) {
-    static cplx<T>* table = nullptr;
-    if (!table) {
-        if (cudaMalloc(&table, W * sizeof(cplx<T>)) != cudaSuccess) return nullptr;
-        twiddle_kernel<T, W><<<(W + 255) / 256, 256, 0, st>>>(table);
+    static cplx<T>* table[kMaxDevices] = {};
+    static std::mutex mu;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!table[dev]) {
+        cplx<T>* t = nullptr;
+        if (cudaMalloc(&t, W * sizeof(cplx<T>)) != cudaSuccess) return nullptr;
+        twiddle_kernel<T, W><<<(W + 255) / 256, 256, 0, st>>>(t);
         count();
+        table[dev] = t;
     }
-    return table;
+    return table[dev];
 }
 
 }  // namespace pty
