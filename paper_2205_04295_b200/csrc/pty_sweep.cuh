@@ -72,10 +72,10 @@ template <typename T, int W>
 __host__ __device__ constexpr size_t sweep_smem_phase(int threads) {
     constexpr int B = Shape<W>::B, TEAM = 4 * B, XS = xch_size<W>(), LS4 = team_line_stride<W>();
     const int ngroups = threads / B, nteams = threads / TEAM;
-    const size_t p1 = (size_t)ngroups * XS * sizeof(cplx<T>) + (size_t)nteams * W * 5 * sizeof(cplx<T>) +
+    const size_t p1 = (size_t)ngroups * XS * sizeof(cplx<T>) + (size_t)nteams * W * 4 * sizeof(cplx<T>) +
                       (size_t)nteams * 4 * sizeof(T);
-    const size_t p4 = (size_t)nteams * 4 * LS4 * sizeof(cplx<T>) +
-                      (size_t)nteams * 4 * W * (sizeof(cplx<T>) + 2 * sizeof(T)) + (size_t)nteams * 4 * sizeof(T);
+    const size_t p4 = (size_t)nteams * 4 * LS4 * sizeof(cplx<T>) + (size_t)nteams * 4 * W * sizeof(cplx<T>) +
+                      (size_t)nteams * 4 * acc_stride<W>() * 2 * sizeof(T) + (size_t)nteams * 4 * sizeof(T);
     return p1 > p4 ? p1 : p4;
 }
 
@@ -182,16 +182,15 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
     // phase-region views
     C* xch = reinterpret_cast<C*>(region) + grp * XS;                          // P1-P3
     C* res = reinterpret_cast<C*>(region) + (size_t)grp * P.M * XS;            // P2-P3 resident lines
-    C* tt = reinterpret_cast<C*>(region) + (size_t)NGRP * XS + (size_t)team * W * 5;   // P1
-    T* red4_p1 = reinterpret_cast<T*>(reinterpret_cast<C*>(region) + (size_t)NGRP * XS + (size_t)NTEAM * W * 5) + team * 4;
+    C* tt = reinterpret_cast<C*>(region) + (size_t)NGRP * XS + (size_t)team * W * 4;   // P1
+    T* red4_p1 = reinterpret_cast<T*>(reinterpret_cast<C*>(region) + (size_t)NGRP * XS + (size_t)NTEAM * W * 4) + team * 4;
     C* lines = reinterpret_cast<C*>(region) + (size_t)team * 4 * LS4;                  // P4
     C* numer = reinterpret_cast<C*>(region) + (size_t)NTEAM * 4 * LS4 + (size_t)team * 4 * W;
-    T* ppacc = reinterpret_cast<T*>(reinterpret_cast<C*>(region) + (size_t)NTEAM * 4 * LS4 + (size_t)NTEAM * 4 * W) +
-               (size_t)team * 4 * W;
-    T* nppacc = reinterpret_cast<T*>(reinterpret_cast<C*>(region) + (size_t)NTEAM * 4 * LS4 + (size_t)NTEAM * 4 * W) +
-                (size_t)NTEAM * 4 * W + (size_t)team * 4 * W;
-    T* red4_p4 = reinterpret_cast<T*>(reinterpret_cast<C*>(region) + (size_t)NTEAM * 4 * LS4 + (size_t)NTEAM * 4 * W) +
-                 (size_t)2 * NTEAM * 4 * W + team * 4;
+    constexpr int RS = acc_stride<W>();
+    T* acc_base = reinterpret_cast<T*>(reinterpret_cast<C*>(region) + (size_t)NTEAM * 4 * LS4 + (size_t)NTEAM * 4 * W);
+    T* ppacc = acc_base + (size_t)team * 4 * RS;
+    T* nppacc = acc_base + (size_t)NTEAM * 4 * RS + (size_t)team * 4 * RS;
+    T* red4_p4 = acc_base + (size_t)2 * NTEAM * 4 * RS + team * 4;
 
     GridBarrier bar{P.barrier, 0u};
     auto phase_sync = [&]() {

@@ -51,6 +51,15 @@ template <int W> __host__ __device__ constexpr int team_line_stride() {
     return ((W + W / Shape<W>::B + 1 + 11) / 16) * 16 + 4;
 }
 
+// transposed staging tile tt[kc][4]: the row slot is XOR-swizzled with
+// (kc / 4) % 4 so both the column-wise writes (16 consecutive kc of one row)
+// and the row-quad reads (4 consecutive kc, all rows) are bank-conflict free
+__device__ __forceinline__ int tt_swz(int kc) { return (kc >> 2) & 3; }
+
+// row stride of the team's real [4][.] accumulators: +16 words puts the two
+// groups of a warp on different banks
+template <int W> __host__ __device__ constexpr int acc_stride() { return W + 16; }
+
 // output column of stage-2 slot q for group lane b
 template <int W> __device__ __forceinline__ int slot_col(int b, int q) {
     constexpr int A = Shape<W>::A, B = Shape<W>::B;
@@ -103,13 +112,13 @@ __device__ __forceinline__ T task_row_fwd(const cplx<T>* tw, cplx<T>* xch, cplx<
     }
     group_fft<T, W, false>(
         xch, tw, b, gmask, [&](int n, int a) { return scale(pv[a] * ov[a], checker<T>(r, n)); },
-        [&](int kc, int, C v) { tt[kc * 5 + gi] = v; });
+        [&](int kc, int, C v) { tt[kc * 4 + (gi ^ tt_swz(kc))] = v; });
     team_sync<TEAM>(team);
     C* dst = dst_pos + m * WW + 4 * rq;
 #pragma unroll
     for (int i = 0; i < 4 * W / TEAM; ++i) {
         const int e = tl + i * TEAM;
-        dst[(size_t)(e >> 2) * W + (e & 3)] = tt[(e >> 2) * 5 + (e & 3)];
+        dst[(size_t)(e >> 2) * W + (e & 3)] = tt[(e >> 2) * 4 + ((e & 3) ^ tt_swz(e >> 2))];
     }
     T res = T(0);
     if (m == 0) res = team_max4<W>(om, red4, team, gi, b);
@@ -280,8 +289,8 @@ __device__ __forceinline__ T task_row_inv_update(const cplx<T>* tw, cplx<T>* lin
     T* pprow = ppg + (size_t)r * W;
     C* myline = lines + gi * LS4;
     C* nrow = numer + gi * W;
-    T* idp = invdp + gi * W;
-    T* npp = nppacc + gi * W;
+    T* idp = invdp + gi * acc_stride<W>();
+    T* npp = nppacc + gi * acc_stride<W>();
     const T dmax_p = beta * omax + (T(1) - beta) * omax;
     C ov[A];
 #pragma unroll
