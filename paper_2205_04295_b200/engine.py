@@ -30,7 +30,7 @@ from pathlib import Path
 import numpy as np
 
 from . import _native
-from .dataio import write_checkpoint
+from .dataio import read_checkpoint, write_checkpoint
 from .errors import ParameterError, ShapeError, raise_for_status
 from .fields import check_window
 from .posref import AdamBuffers, PosRefConfig
@@ -517,6 +517,41 @@ def _refine_positions(st: ReconState, pc: PosRefConfig, n: int, w: int, index=No
                                    dy[s:e], dx[s:e], peak[s:e], ok[s:e])
     # sensors return (gx, gy) = (est.dx, est.dy) (posref.py:63)
     _native.adam_apply(st.positions, st.adam, dx, dy, ok, pc, position_bounds(st, w), index=idx_d)
+
+
+def resume(checkpoint_dir, dataset, config: SolverConfig) -> ReconState:
+    """Rebuild a device-resident ReconState from a checkpoint written by
+    ``run(checkpoint_every=...)`` (dataio.py:164-204 format, plus the Adam
+    buffers this package stores), so a reconstruction continues where it
+    stopped: same visit order (iteration = len(error_trace)), positions and
+    Adam state.  The container stores complex64 fields (as the reference)."""
+    t = _native.torch()
+    ck = read_checkpoint(checkpoint_dir)
+    dev = _native.device()
+    cdt = t.complex128 if config.precision == "fp64" else t.complex64
+    w = dataset.geometry.window
+    chirp = None
+    if config.propagator == "fresnel":
+        from .fields import fresnel_chirp
+        chirp = fresnel_chirp(dataset.geometry, cdt, dev)
+    obj = t.from_numpy(np.ascontiguousarray(ck["object"])).to(dev, cdt)
+    positions = t.from_numpy(np.ascontiguousarray(ck["positions"], np.float64)).to(dev)
+    if positions.shape != (dataset.n_positions, 2):
+        raise ShapeError(f"checkpoint has {positions.shape[0]} positions, dataset {dataset.n_positions}")
+    adam = None
+    if config.posref is not None:
+        if "adam" in ck:
+            m, v, tt = ck["adam"]
+            adam = AdamBuffers(t.from_numpy(np.ascontiguousarray(m)).to(dev),
+                               t.from_numpy(np.ascontiguousarray(v)).to(dev),
+                               t.from_numpy(np.ascontiguousarray(tt, np.int64)).to(dev))
+        else:
+            adam = AdamBuffers.zeros(dataset.n_positions, dev)
+    st = ReconState(obj=obj, probes=t.zeros((len(ck["probes"]), w, w), dtype=cdt, device=dev),
+                    positions=positions, canvas_origin=ck["canvas_origin"], adam=adam,
+                    error_trace=ck["error_trace"], frame_chirp=chirp)
+    st.probes = [np.asarray(p) for p in ck["probes"]]
+    return st
 
 
 def run(dataset, config: SolverConfig, state: ReconState | None = None,

@@ -163,3 +163,20 @@ def test_run_and_checkpointing(gpu, tmp_path):
     last = dataio.read_checkpoint(tmp_path / "iter_0004")
     np.testing.assert_array_equal(last["positions"], host(st.positions))
     np.testing.assert_array_equal(last["adam"][2], host(st.adam.t))
+
+
+def test_resume_from_checkpoint_continues_the_run(gpu, tmp_path):
+    """run 4 sweeps with checkpoints, resume from iteration 2 and sweep twice:
+    same visit orders, positions and Adam counters as the uninterrupted run;
+    fields within complex64 container rounding."""
+    _, _, _, ds = scene(jitter=1.0)
+    cfg = pk.SolverConfig(iterations=4, posref=pk.PosRefConfig(warmup_iterations=1, kappa=10))
+    full = pk.run(ds, cfg, checkpoint_every=2, checkpoint_dir=tmp_path)
+    st = pk.resume(tmp_path / "iter_0002", ds, cfg)
+    assert st.iteration == 2
+    for _ in range(2):
+        pk.sweep(st, ds, cfg)
+    np.testing.assert_array_equal(host(st.adam.t), host(full.adam.t))
+    np.testing.assert_allclose(host(st.positions), host(full.positions), atol=1e-6)
+    np.testing.assert_allclose(host(st.obj), host(full.obj), atol=1e-5)
+    np.testing.assert_allclose(st.error_trace, full.error_trace, rtol=1e-4)
