@@ -390,6 +390,26 @@ def sweep_batched(state: ReconState, dataset, config: SolverConfig, group=None) 
     return st
 
 
+_REPLICA_BUFS: dict = {}
+
+
+def _replica_buffers(r: int, n: int) -> dict:
+    """Per (device, stream, R, N) pinned + device buffers of sweep_replicas."""
+    t = _native.torch()
+    dev = _native.device()
+    key = (dev.index, t.cuda.current_stream(dev).cuda_stream, r, n)
+    b = _REPLICA_BUFS.get(key)
+    if b is None:
+        b = {"order_h": t.empty((r, n), dtype=t.int32, pin_memory=True),
+             "order_d": t.empty((r, n), dtype=t.int32, device=dev),
+             "status_d": t.empty((r,), dtype=t.int32, device=dev),
+             "status_h": t.empty((r,), dtype=t.int32, pin_memory=True),
+             "err_d": t.empty((r, 3), dtype=t.float64, device=dev),
+             "err_h": t.empty((r, 3), dtype=t.float64, pin_memory=True)}
+        _REPLICA_BUFS[key] = b
+    return b
+
+
 def sweep_replicas(states, datasets, config: SolverConfig, orders=None, kernel_events=None):
     """Advance K independent reconstructions by one sweep each in ONE launch.
 
@@ -423,20 +443,32 @@ def sweep_replicas(states, datasets, config: SolverConfig, orders=None, kernel_e
         sense = _native.SENSE_XCORR_A if config.posref.sensor == "XCORR_A" else _native.SENSE_XCORR_B
     slots = (_native.PtySlot * len(states))()
     keep = []
+    R = len(states)
+    # one pinned/device buffer set for the whole replica set: a single H2D
+    # of every visit order, one memset of the status words, one D2H of every
+    # error triple and status after the launch (instead of 4 tiny copies or
+    # kernels per replica on the host's critical path)
+    rb = _replica_buffers(R, n)
+    perms = {}
     for k, (st, ds) in enumerate(zip(states, datasets)):
         if ds.geometry.window != w or ds.n_positions != n or st.window != w or st.obj.dtype != cdt \
                 or st.probe_stack.shape[0] != m:
             raise ShapeError("replicas must share window, mode count, positions and precision")
+        if orders is not None:
+            rb["order_h"].numpy()[k] = orders[k]
+        else:                                  # one permutation per distinct iteration count
+            it = st.iteration
+            if it not in perms:
+                perms[it] = visit_order(n, config, it)
+            rb["order_h"].numpy()[k] = perms[it]
+    rb["order_d"].copy_(rb["order_h"], non_blocking=True)
+    rb["status_d"].zero_()
+    for k, (st, ds) in enumerate(zip(states, datasets)):
         pats = device_patterns(ds, rdt)
         pats_t = device_patterns_t(ds, rdt)
-        order = orders[k] if orders is not None else visit_order(n, config, st.iteration)
-        order_h = st.buffer("order", (n,), t.int32, pinned=True)
-        order_h.numpy()[:] = order
-        order_d = st.buffer("order", (n,), t.int32)
-        order_d.copy_(order_h, non_blocking=True)
-        status = st.buffer("status", (1,), t.int32)
-        status.zero_()
-        err = st.buffer("err", (3,), t.float64)
+        order_d = rb["order_d"][k]
+        status = rb["status_d"][k:k + 1]
+        err = rb["err_d"][k]
         stage = st.buffer("stage", (n, 2, w, w), cdt) if sense != _native.SENSE_NONE else None
         st.obj = st.obj.contiguous()
         st.probe_stack = st.probe_stack.contiguous()
@@ -467,17 +499,13 @@ def sweep_replicas(states, datasets, config: SolverConfig, orders=None, kernel_e
                 and (st.iteration + 1) % config.ortho_interval == 0):
             _native.orthogonalize(st.probe_stack)
 
-    hosts = []
-    for st in states:
-        he = st.buffer("err", (3,), t.float64, pinned=True)
-        hs = st.buffer("status", (1,), t.int32, pinned=True)
-        he.copy_(st.buffer("err", (3,), t.float64), non_blocking=True)
-        hs.copy_(st.buffer("status", (1,), t.int32), non_blocking=True)
-        hosts.append((he, hs))
+    rb["err_h"].copy_(rb["err_d"], non_blocking=True)
+    rb["status_h"].copy_(rb["status_d"], non_blocking=True)
     t.cuda.current_stream().synchronize()
     dt = time.perf_counter() - t0
+    err_h, status_h = rb["err_h"].numpy(), rb["status_h"].numpy()
     for k, st in enumerate(states):
-        (num, den, worst), status = hosts[k][0].numpy(), hosts[k][1].numpy()[0]
+        (num, den, worst), status = err_h[k], status_h[k]
         raise_for_status(int(status), f"sweep, replica {k}")
         st.error_trace.append(float(num) / max(float(den), TINY))
         if config.track_modulus_error:
