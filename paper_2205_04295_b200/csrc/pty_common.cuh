@@ -75,12 +75,6 @@ template <typename T> __device__ __forceinline__ cplx<T> divr(cplx<T> a, T d) {
     return {a.re * inv, a.im * inv};
 }
 
-// Hide a value from loop-invariant code motion: the compiler otherwise hoists
-// per-element reciprocals out of the mode loop and spills them to local
-// memory (measured: the reload stalls dominated the row-update phase).
-__device__ __forceinline__ void opaque(float& x) { asm volatile("" : "+f"(x)); }
-__device__ __forceinline__ void opaque(double& x) { asm volatile("" : "+d"(x)); }
-
 template <typename T> struct real_limits;
 template <> struct real_limits<float>  { static __device__ __forceinline__ float tiny() { return 1.17549435e-38f; } };
 template <> struct real_limits<double> { static __device__ __forceinline__ double tiny() { return 2.2250738585072014e-308; } };
