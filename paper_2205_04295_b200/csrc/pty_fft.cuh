@@ -15,6 +15,7 @@
 // Forward = exp(-2 pi i k n / W) unnormalised (np.fft.fft), inverse =
 // exp(+2 pi i k n / W) unnormalised (np.fft.ifft * W); callers scale.
 #pragma once
+#include <type_traits>
 #include "pty_common.cuh"
 
 namespace pty {
@@ -114,6 +115,36 @@ __device__ __forceinline__ void load_twiddles(cplx<T>* tw_smem, const cplx<T>* t
     for (int i = threadIdx.x; i < W; i += blockDim.x) tw_smem[i] = tw_global[i];
 }
 
+// Inter-stage twiddles v[k1] *= w^(b k1) (conjugate for the inverse).
+// float: w(4q + r) = w(4q) * w(r) from 3 + A/4 - 1 table reads instead of
+// A - 1 (the twiddle reads were 14 % of all shared-memory wavefronts of the
+// sweep); the product adds ~1 ulp.  double: straight table reads.
+template <typename T, int W, bool INV>
+__device__ __forceinline__ void apply_twiddles(cplx<T>* v, const cplx<T>* tw, int b) {
+    constexpr int A = Shape<W>::A, B = Shape<W>::B;
+    if constexpr (std::is_same<T, float>::value && A >= 8) {
+        cplx<T> wr[4], wq[A / 4];
+        wr[0] = cplx<T>{T(1), T(0)};
+        wq[0] = cplx<T>{T(1), T(0)};
+#pragma unroll
+        for (int r = 1; r < 4; ++r) wr[r] = tw[r * B + b];
+#pragma unroll
+        for (int q = 1; q < A / 4; ++q) wq[q] = tw[4 * q * B + b];
+#pragma unroll
+        for (int k1 = 1; k1 < A; ++k1) {
+            const int q = k1 / 4, r = k1 % 4;
+            const cplx<T> w = r == 0 ? wq[q] : (q == 0 ? wr[r] : wq[q] * wr[r]);
+            v[k1] = INV ? mulc(v[k1], w) : v[k1] * w;
+        }
+    } else {
+#pragma unroll
+        for (int k1 = 1; k1 < A; ++k1) {
+            const cplx<T> w = tw[k1 * B + b];
+            v[k1] = INV ? mulc(v[k1], w) : v[k1] * w;
+        }
+    }
+}
+
 // Transform one padded line in shared memory with a group of B threads.
 // b = thread index in the group, mask = the group's lanes.
 template <typename T, int W, bool INV>
@@ -123,11 +154,7 @@ __device__ __forceinline__ void line_fft(cplx<T>* line, const cplx<T>* tw, int b
 #pragma unroll
     for (int a = 0; a < A; ++a) v[a] = line[a * (B + 1) + b];
     DFT<T, A, INV>::run(v);
-#pragma unroll
-    for (int k1 = 1; k1 < A; ++k1) {
-        const cplx<T> w = tw[k1 * B + b];
-        v[k1] = INV ? mulc(v[k1], w) : v[k1] * w;
-    }
+    apply_twiddles<T, W, INV>(v, tw, b);
     __syncwarp(mask);
 #pragma unroll
     for (int k1 = 0; k1 < A; ++k1) line[k1 * (B + 1) + b] = v[k1];
@@ -164,11 +191,7 @@ __device__ __forceinline__ void group_fft(cplx<T>* xch, const cplx<T>* tw, int b
 #pragma unroll
     for (int a = 0; a < A; ++a) v[a] = load(B * a + b, a);
     DFT<T, A, INV>::run(v);
-#pragma unroll
-    for (int k1 = 1; k1 < A; ++k1) {
-        const cplx<T> w = tw[k1 * B + b];
-        v[k1] = INV ? mulc(v[k1], w) : v[k1] * w;
-    }
+    apply_twiddles<T, W, INV>(v, tw, b);
     __syncwarp(mask);
 #pragma unroll
     for (int k1 = 0; k1 < A; ++k1) xch[k1 * (B + 1) + b] = v[k1];
