@@ -45,6 +45,7 @@ struct SweepDev {
     double alpha_o, alpha_p, beta, gamma, eps_rel;
     int update_probe, track_mod, sense;
     int resident;                 // P2 -> P3 column lines stay in shared memory (<= 1 column task per group)
+    int p4_staged;                // P4: all modes' lines staged in shared memory, element-linear epilogue
     // workspace
     unsigned int* barrier;
     int* anchors;                 // [nslots][N][2]
@@ -321,11 +322,27 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
                 continue;
             }
             C* stg = P.sense == PTY_SENSE_XCORR_A ? reinterpret_cast<C*>(sl.stage) + (size_t)j * 2 * WW : nullptr;
-            const T npk = task_row_inv_update<T, W>(tw, lines, numer, ppacc, nppacc, red4_p4, team, tl, gi, b, gmask,
-                                                    scratch + (size_t)s * M * WW, M, rq, reinterpret_cast<C*>(sl.obj),
-                                                    reinterpret_cast<T*>(P.ppg) + (size_t)s * WW,
-                                                    sl.Wc, s_ar[s], s_ac[s], reinterpret_cast<C*>(sl.probes), peak,
-                                                    omax, U, stg);
+            T npk;
+            if (P.p4_staged) {
+                C* lines_m = reinterpret_cast<C*>(region) + (size_t)team * M * 4 * LS4;
+                T* red4_s = reinterpret_cast<T*>(reinterpret_cast<C*>(region) + (size_t)NTEAM * M * 4 * LS4) + team * 4;
+#define PTY_P4S(MM) npk = task_row_inv_update_staged<T, W, MM>(tw, lines_m, red4_s, team, tl, gi, b, gmask, \
+                    scratch + (size_t)s * M * WW, rq, reinterpret_cast<C*>(sl.obj), reinterpret_cast<T*>(P.ppg) + (size_t)s * WW, \
+                    sl.Wc, s_ar[s], s_ac[s], reinterpret_cast<C*>(sl.probes), peak, omax, U, stg)
+                switch (M) {
+                    case 1: PTY_P4S(1); break;
+                    case 2: PTY_P4S(2); break;
+                    case 3: PTY_P4S(3); break;
+                    default: PTY_P4S(4); break;   // host enables staging only for M <= 4
+                }
+#undef PTY_P4S
+            } else {
+                npk = task_row_inv_update<T, W>(tw, lines, numer, ppacc, nppacc, red4_p4, team, tl, gi, b, gmask,
+                                                scratch + (size_t)s * M * WW, M, rq, reinterpret_cast<C*>(sl.obj),
+                                                reinterpret_cast<T*>(P.ppg) + (size_t)s * WW,
+                                                sl.Wc, s_ar[s], s_ac[s], reinterpret_cast<C*>(sl.probes), peak,
+                                                omax, U, stg);
+            }
             if (tl == 0) peak_part[((size_t)((step + 1) & 1) * P.nslots + s) * nq + rq] = npk;
         }
         stamp(step, 4);

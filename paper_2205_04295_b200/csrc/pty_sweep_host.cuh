@@ -105,7 +105,14 @@ int run_sweep_lines(const PtySweepArgs* a, cudaStream_t st) {
     const bool res_fit = 2 * (sweep_smem_fixed<T, W>() + res_phase + 1024) <= max_smem_per_sm();
     const int grid_ctas = sm_count() * kSweepMaxCtasPerSm;
     P.resident = (want_res && res_fit && (long)S * W <= (long)grid_ctas * NGRP && env_int("PTY_CLUSTER", 0) == 0) ? 1 : 0;
-    const size_t smem = sweep_smem_fixed<T, W>() + (P.resident ? res_phase : base_phase);
+    // P4 staged: M*4 padded lines per team (M <= 4)
+    constexpr int NTEAM4 = kSweepThreads / (4 * Shape<W>::B);
+    const size_t p4s_bytes = (size_t)NTEAM4 * M * 4 * team_line_stride<W>() * sizeof(cplx<T>) + NTEAM4 * 4 * sizeof(T);
+    size_t phase = P.resident ? res_phase : base_phase;
+    const bool p4s_fit = 2 * (sweep_smem_fixed<T, W>() + std::max(phase, p4s_bytes) + 1024) <= max_smem_per_sm();
+    P.p4_staged = (env_int("PTY_P4_STAGED", 1) && M <= 4 && p4s_fit) ? 1 : 0;
+    if (P.p4_staged) phase = std::max(phase, p4s_bytes);
+    const size_t smem = sweep_smem_fixed<T, W>() + phase;
     if (smem > max_dyn_smem()) return PTY_ERR_ARGUMENT;
     int K = std::max(0, env_int("PTY_CLUSTER", 0));
     int grid = 0;

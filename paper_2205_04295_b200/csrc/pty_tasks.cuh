@@ -370,4 +370,112 @@ __device__ __forceinline__ T task_row_inv_update(const cplx<T>* tw, cplx<T>* lin
     return team_max4<W>(pk, red4, team, gi, b);
 }
 
+// Row pass 2, staged variant (shared memory for all modes): team task (row
+// quad rq) of one position.  (1) the 4 rows of every mode are loaded into the
+// team's lines (lines[(m*4 + gi)*LS4 + pad(c)]), (2) every line is
+// inverse-transformed in place, (3) the update epilogue runs element-linear
+// over the team with all of an element's inputs (o, sum|P|^2, P_m, psi'_m)
+// gathered first and its accumulators in registers.  Same expressions and
+// mode order as task_row_inv_update (engine.py:119-150, 218-224,
+// fields.py:101-107).  Returns the team max of the next visit's sum_m |P_m|^2.
+template <typename T, int W, int MODES>
+__device__ __forceinline__ T task_row_inv_update_staged(const cplx<T>* tw, cplx<T>* lines, T* red4, int team,
+                                                        int tl, int gi, int b, unsigned gmask, const cplx<T>* pos,
+                                                        int rq, cplx<T>* obj, T* ppg, int Wc, int ar, int ac,
+                                                        cplx<T>* probes, T peak, T omax, const UpdateParams& U,
+                                                        cplx<T>* stg) {
+    using C = cplx<T>;
+    constexpr int B = Shape<W>::B, TEAM = 4 * B, LS4 = team_line_stride<W>(), NE = 4 * W / TEAM;
+    constexpr int CH = MODES <= 3 ? 4 : (MODES <= 6 ? 2 : 1);
+    const size_t WW = (size_t)W * W;
+    const T invW2 = T(1) / (T(W) * T(W));
+    const T alpha_o = T(U.alpha_o), alpha_p = T(U.alpha_p), beta = T(U.beta), gamma = T(U.gamma),
+            eps_rel = T(U.eps_rel);
+    // the scratch rows of mode m+1 are in flight before mode m is stored to
+    // shared memory (two modes of loads outstanding per thread)
+    C cur[NE], nxt[NE];
+#pragma unroll
+    for (int i = 0; i < NE; ++i) {
+        const int e = tl + i * TEAM;
+        cur[i] = pos[(size_t)(e >> 2) * W + 4 * rq + (e & 3)];
+    }
+    team_sync<TEAM>(team);                                     // lines free
+#pragma unroll
+    for (int m = 0; m < MODES; ++m) {
+        if (m + 1 < MODES) {
+#pragma unroll
+            for (int i = 0; i < NE; ++i) {
+                const int e = tl + i * TEAM;
+                nxt[i] = pos[(m + 1) * WW + (size_t)(e >> 2) * W + 4 * rq + (e & 3)];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < NE; ++i) {
+            const int e = tl + i * TEAM;
+            lines[(m * 4 + (e & 3)) * LS4 + pad<W>(e >> 2)] = cur[i];
+        }
+        if (m + 1 < MODES) {
+#pragma unroll
+            for (int i = 0; i < NE; ++i) cur[i] = nxt[i];
+        }
+    }
+    team_sync<TEAM>(team);
+#pragma unroll 1
+    for (int m = 0; m < MODES; ++m) line_fft<T, W, true>(lines + (m * 4 + gi) * LS4, tw, b, gmask);
+    team_sync<TEAM>(team);
+    const T dmax_p = beta * omax + (T(1) - beta) * omax;
+    const T dmax_o = gamma * peak + (T(1) - gamma) * peak;
+    T pk = T(0);
+#pragma unroll 1
+    for (int h = 0; h < NE; h += CH) {
+        C ov[CH], pv[MODES][CH];
+        T ppv[CH];
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+            const int e = tl + (h + k) * TEAM, rr = e / W, c = e % W, r = 4 * rq + rr;
+            ov[k] = obj[(size_t)(ar + r) * Wc + ac + c];
+            ppv[k] = ppg[(size_t)r * W + c];
+#pragma unroll
+            for (int m = 0; m < MODES; ++m) pv[m][k] = probes[m * WW + (size_t)r * W + c];
+        }
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+            const int e = tl + (h + k) * TEAM, rr = e / W, c = e % W, r = 4 * rq + rr;
+            const C o = ov[k];
+            T dp = beta * omax + (T(1) - beta) * norm2(o);
+            dp = dp + eps_rel * dmax_p;
+            const T idp = T(1) / dp;
+            C numer{T(0), T(0)};
+            T npp = T(0);
+#pragma unroll
+            for (int m = 0; m < MODES; ++m) {
+                const C X = lines[(m * 4 + rr) * LS4 + pad<W>(c)];
+                const C d = scale(X, checker<T>(r, c) * invW2) - pv[m][k] * o;
+                numer = numer + mulc(d, pv[m][k]);
+                if (U.update_probe) {
+                    const C np_ = pv[m][k] + scale(mulc(scale(d, alpha_p), o), idp);
+                    probes[m * WW + (size_t)r * W + c] = np_;
+                    npp += norm2(np_);
+                }
+            }
+            T den = gamma * peak + (T(1) - gamma) * ppv[k];
+            den = den + eps_rel * dmax_o;
+            const C no = o + divr(scale(numer, alpha_o), den);
+            obj[(size_t)(ar + r) * Wc + ac + c] = o + (no - o);          // paste_add_inplace
+            if (stg) {
+                stg[(size_t)r * W + c] = o;
+                stg[WW + (size_t)r * W + c] = no;
+            }
+            if (U.update_probe) {
+                ppg[(size_t)r * W + c] = npp;
+                pk = fmax(pk, npp);
+            } else {
+                pk = fmax(pk, ppv[k]);
+            }
+        }
+    }
+    pk = group_max<B>(pk);
+    return team_max4<W>(pk, red4, team, gi, b);
+}
+
 }  // namespace pty
