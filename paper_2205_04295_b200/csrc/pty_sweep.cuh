@@ -46,6 +46,7 @@ struct SweepDev {
     int update_probe, track_mod, sense;
     int resident;                 // P2 -> P3 column lines stay in shared memory (<= 1 column task per group)
     int p4_staged;                // P4: all modes' lines staged in shared memory, element-linear epilogue
+    int p1_staged;                // P1: one task per row quad for all modes (needs p4_staged's shared memory)
     // workspace
     unsigned int* barrier;
     int* anchors;                 // [nslots][N][2]
@@ -248,6 +249,33 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
         }
         __syncthreads();
         // ---------------------------------------------------------- P1 rows
+        if (P.p4_staged && P.p1_staged) {
+            C* lines_m = reinterpret_cast<C*>(region) + (size_t)team * M * 4 * LS4;
+            T* red4_s = reinterpret_cast<T*>(reinterpret_cast<C*>(region) + (size_t)NTEAM * M * 4 * LS4) + team * 4;
+            for (int task = cta * NTEAM + team; task < S * nq; task += ncta * NTEAM) {
+                const int s = s0 + task / nq, rq = task % nq;
+                if (s_dead[s]) continue;
+                const SlotDev& sl = P.slot[s];
+                const int j = s_j[s];
+                const char* It = reinterpret_cast<const char*>(reinterpret_cast<const T*>(sl.patterns_t) + (size_t)j * WW +
+                                                               (size_t)4 * rq * W);
+                for (int q = tl; q < (int)(4 * W * sizeof(T) / 128); q += TEAM)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(It + q * 128));
+                C* stg = P.sense == PTY_SENSE_XCORR_A ? reinterpret_cast<C*>(sl.stage) + (size_t)j * 2 * WW : nullptr;
+                T om;
+#define PTY_P1S(MM) om = task_row_fwd_staged<T, W, MM>(tw, lines_m, red4_s, team, tl, gi, b, gmask, \
+                    reinterpret_cast<const C*>(sl.obj), sl.Wc, s_ar[s], s_ac[s], reinterpret_cast<const C*>(sl.probes), rq, \
+                    scratch + (size_t)s * M * WW, stg)
+                switch (M) {
+                    case 1: PTY_P1S(1); break;
+                    case 2: PTY_P1S(2); break;
+                    case 3: PTY_P1S(3); break;
+                    default: PTY_P1S(4); break;
+                }
+#undef PTY_P1S
+                if (tl == 0) omax_part[(size_t)s * nq + rq] = om;
+            }
+        } else
         for (int task = cta * NTEAM + team; task < S * M * nq; task += ncta * NTEAM) {
             const int s = s0 + task / (M * nq), m = (task / nq) % M, rq = task % nq;
             if (s_dead[s]) continue;

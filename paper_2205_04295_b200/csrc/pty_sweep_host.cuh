@@ -112,6 +112,7 @@ int run_sweep_lines(const PtySweepArgs* a, cudaStream_t st) {
     const bool p4s_fit = 2 * (sweep_smem_fixed<T, W>() + std::max(phase, p4s_bytes) + 1024) <= max_smem_per_sm();
     P.p4_staged = (env_int("PTY_P4_STAGED", 1) && M <= 4 && p4s_fit) ? 1 : 0;
     if (P.p4_staged) phase = std::max(phase, p4s_bytes);
+    P.p1_staged = P.p4_staged && env_int("PTY_P1_STAGED", 1);
     const size_t smem = sweep_smem_fixed<T, W>() + phase;
     if (smem > max_dyn_smem()) return PTY_ERR_ARGUMENT;
     int K = std::max(0, env_int("PTY_CLUSTER", 0));

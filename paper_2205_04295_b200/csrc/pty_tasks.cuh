@@ -126,6 +126,67 @@ __device__ __forceinline__ T task_row_fwd(const cplx<T>* tw, cplx<T>* xch, cplx<
     return res;
 }
 
+// Row pass, staged variant: team task (row quad rq, ALL modes) of one
+// position.  The object rows are loaded once and kept in registers; for each
+// mode the probe row is loaded, the exit wave staged in the team's lines
+// (lines[(m*4 + gi)*LS4 + pad(n)]); then every line is transformed in place
+// and written transposed ([m][kc][r]) straight from the lines.  Same
+// arithmetic as task_row_fwd.  Returns the team's max|o|^2.
+template <typename T, int W, int MODES>
+__device__ __forceinline__ T task_row_fwd_staged(const cplx<T>* tw, cplx<T>* lines, T* red4, int team, int tl, int gi,
+                                                 int b, unsigned gmask, const cplx<T>* obj, int Wc, int ar, int ac,
+                                                 const cplx<T>* probes, int rq, cplx<T>* dst_pos, cplx<T>* stg_o) {
+    using C = cplx<T>;
+    constexpr int A = Shape<W>::A, B = Shape<W>::B, TEAM = 4 * B, LS4 = team_line_stride<W>();
+    const size_t WW = (size_t)W * W;
+    const int r = 4 * rq + gi;
+    const C* orow = obj + (size_t)(ar + r) * Wc + ac;
+    const C* prow = probes + (size_t)r * W;
+    C ov[A], pv[A];
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+        ov[a] = orow[B * a + b];
+        pv[a] = prow[B * a + b];
+    }
+    T om = T(0);
+#pragma unroll
+    for (int a = 0; a < A; ++a) om = fmax(om, norm2(ov[a]));
+    if (stg_o) {
+        C* stg = stg_o + (size_t)r * W;
+#pragma unroll
+        for (int a = 0; a < A; ++a) stg[B * a + b] = ov[a];
+    }
+    team_sync<TEAM>(team);                                    // lines free
+#pragma unroll
+    for (int m = 0; m < MODES; ++m) {
+        if (m > 0) {
+#pragma unroll
+            for (int a = 0; a < A; ++a) pv[a] = prow[m * WW + B * a + b];
+        }
+        C* line = lines + (m * 4 + gi) * LS4;
+#pragma unroll
+        for (int a = 0; a < A; ++a) {
+            const int n = B * a + b;
+            line[pad<W>(n)] = scale(pv[a] * ov[a], checker<T>(r, n));
+        }
+    }
+    __syncwarp(gmask);
+#pragma unroll 1
+    for (int m = 0; m < MODES; ++m) line_fft<T, W, false>(lines + (m * 4 + gi) * LS4, tw, b, gmask);
+    team_sync<TEAM>(team);
+#pragma unroll
+    for (int m = 0; m < MODES; ++m) {
+        C* dst = dst_pos + m * WW + 4 * rq;
+        const C* lm = lines + m * 4 * LS4;
+#pragma unroll
+        for (int i = 0; i < 4 * W / TEAM; ++i) {
+            const int e = tl + i * TEAM;
+            dst[(size_t)(e >> 2) * W + (e & 3)] = lm[(e & 3) * LS4 + pad<W>(e >> 2)];
+        }
+    }
+    return team_max4<W>(om, red4, team, gi, b);
+}
+
 // Column pass, group task (column kc) of one position: forward column DFTs of
 // every mode written back in place (Psi), total = sum_m |Psi_m|^2 (engine.py:
 // 114-116) stored transposed; returns the column's max(total).
