@@ -82,6 +82,33 @@ template <> struct real_limits<double> { static __device__ __forceinline__ doubl
 __device__ __forceinline__ float  sqrt_rn(float x)  { return __fsqrt_rn(x); }
 __device__ __forceinline__ double sqrt_rn(double x) { return __dsqrt_rn(x); }
 
+// Throughput forms for the fp32 path (the fp64 instantiation stays
+// correctly rounded, it is the parity path): MUFU square root / reciprocal
+// square root / reciprocal, a few ulp, no IEEE slow-path branches.
+__device__ __forceinline__ float sqrt_fast(float x) {
+    float y;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ double sqrt_fast(double x) { return __dsqrt_rn(x); }
+__device__ __forceinline__ float rsqrt_fast(float x) {
+    float y;
+    asm("rsqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ double rsqrt_fast(double x) { return 1.0 / __dsqrt_rn(x); }
+// the modulus-constraint scale sqrt(I) / sqrt(total + eps) (engine.py:118):
+// fp32 multiplies by the MUFU reciprocal square root, fp64 keeps numpy's
+// correctly rounded quotient
+__device__ __forceinline__ float  modulus_scale(float sI, float x)   { return sI * rsqrt_fast(x); }
+__device__ __forceinline__ double modulus_scale(double sI, double x) { return sI / __dsqrt_rn(x); }
+__device__ __forceinline__ float rcp_fast(float x) {
+    float y;
+    asm("rcp.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ double rcp_fast(double x) { return 1.0 / x; }
+
 template <typename T> __device__ __forceinline__ T warp_max(T v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));

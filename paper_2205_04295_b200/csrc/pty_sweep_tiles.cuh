@@ -277,9 +277,9 @@ struct SweepCta {
             T tot = T(0);
             for (int m = 0; m < M; ++m) tot += norm2(my[(size_t)(m * P.TC + cc) * LS + pad<W>(r)]) * invW2;
             const T Iv = Ib[u];
-            const T sI = sqrt_rn(Iv);
-            const T sc = sI / sqrt_rn(tot + eps);
-            const T d = sqrt_rn(tot) - sI;
+            const T sI = sqrt_fast(Iv);
+            const T sc = modulus_scale(sI, tot + eps);
+            const T d = sqrt_fast(tot) - sI;
             enum_ += (double)(d * d);
             eden += (double)Iv;
             T after = T(0);
@@ -401,12 +401,13 @@ struct SweepCta {
                 const T op = norm2(o);
                 T dp = beta * omax + (T(1) - beta) * op;
                 dp = dp + eps_rel * dmax_p;
+                const T idp = rcp_fast(dp);                          // divr multiplies by 1/dp
                 T npp = T(0);
                 for (int m = 0; m < M; ++m) {   // pre-update probes and o_j (engine.py:218-223)
                     const size_t pi = m * WW + (size_t)rr * W + c;
                     const C pv = probes[pi];
                     const C psi = scale(tile[(size_t)((m << P.lgTR) + r) * LS + pad<W>(c)], sg);
-                    const C np_ = pv + divr(mulc(scale(psi - pv * o, alpha_p), o), dp);
+                    const C np_ = pv + scale(mulc(scale(psi - pv * o, alpha_p), o), idp);
                     probes[pi] = np_;
                     npp += norm2(np_);
                 }

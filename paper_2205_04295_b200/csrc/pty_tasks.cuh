@@ -257,9 +257,9 @@ __device__ __forceinline__ void task_col_mod(const cplx<T>* tw, cplx<T>* xch, in
     for (int a = 0; a < A; ++a) {
         const int u = B * a + b;
         const T Iv = It[u], tv = tt[u];
-        const T sI = sqrt_rn(Iv);
-        sc[a] = sI / sqrt_rn(tv + eps);
-        const T d = sqrt_rn(tv) - sI;
+        const T sI = sqrt_fast(Iv);
+        sc[a] = modulus_scale(sI, tv + eps);
+        const T d = sqrt_fast(tv) - sI;
         en += (double)(d * d);
         ed += (double)Iv;
         after[a] = T(0);
@@ -365,7 +365,7 @@ __device__ __forceinline__ T task_row_inv_update(const cplx<T>* tw, cplx<T>* lin
         // one reciprocal per element (divr multiplies by it, numpy's complex/real)
         T dp = beta * omax + (T(1) - beta) * norm2(ov[q]);
         dp = dp + eps_rel * dmax_p;
-        idp[c] = T(1) / dp;
+        idp[c] = rcp_fast(dp);
     }
     for (int m = 0; m < M; ++m) {
         team_sync<TEAM>(team);
@@ -505,7 +505,7 @@ __device__ __forceinline__ T task_row_inv_update_staged(const cplx<T>* tw, cplx<
             const C o = ov[k];
             T dp = beta * omax + (T(1) - beta) * norm2(o);
             dp = dp + eps_rel * dmax_p;
-            const T idp = T(1) / dp;
+            const T idp = rcp_fast(dp);
             C numer{T(0), T(0)};
             T npp = T(0);
 #pragma unroll
