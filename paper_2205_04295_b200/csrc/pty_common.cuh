@@ -64,6 +64,36 @@ __device__ __forceinline__ cplx<float> rot_const(cplx<float> x, float c, float s
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(z) : "l"(f2pack(x.im, x.re)), "l"(f2pack(-s, s)), "l"(t));
     return f2unpack(z);
 }
+// Repeated multiplication by one complex factor o (x * o and x * conj(o)),
+// e.g. the pre-update object value in the update epilogue.  float: the sign
+// pairs are formed once, each product is one FMUL2 + one FFMA2.
+template <typename T> struct OMul {
+    cplx<T> o;
+    __device__ __forceinline__ explicit OMul(cplx<T> o_) : o(o_) {}
+    __device__ __forceinline__ cplx<T> mul(cplx<T> x) const { return x * o; }
+    __device__ __forceinline__ cplx<T> mulconj(cplx<T> x) const { return mulc(x, o); }
+};
+template <> struct OMul<float> {
+    unsigned long long rr, pn, pc;     // (o.re, o.re), (-o.im, o.im), (o.im, -o.im)
+    __device__ __forceinline__ explicit OMul(cplx<float> o) {
+        rr = f2pack(o.re, o.re);
+        pn = f2pack(-o.im, o.im);
+        pc = f2pack(o.im, -o.im);
+    }
+    __device__ __forceinline__ cplx<float> mul(cplx<float> x) const {   // x * o
+        unsigned long long t, z;
+        asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(f2pack(x.re, x.im)), "l"(rr));
+        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(z) : "l"(f2pack(x.im, x.re)), "l"(pn), "l"(t));
+        return f2unpack(z);
+    }
+    __device__ __forceinline__ cplx<float> mulconj(cplx<float> x) const {   // x * conj(o)
+        unsigned long long t, z;
+        asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(f2pack(x.re, x.im)), "l"(rr));
+        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(z) : "l"(f2pack(x.im, x.re)), "l"(pc), "l"(t));
+        return f2unpack(z);
+    }
+};
+
 template <typename T> __device__ __forceinline__ cplx<T> rot_const(cplx<T> x, T c, T s) {
     return {x.re * c - x.im * s, x.re * s + x.im * c};
 }

@@ -391,7 +391,7 @@ struct SweepCta {
             }
             T den = gamma * peak + (T(1) - gamma) * pp;
             den = den + eps_rel * dmax_o;
-            const C no = o + divr(scale(numer, alpha_o), den);
+            const C no = o + scale(scale(numer, alpha_o), rcp_fast(den));
             obj[oi] = o + (no - o);                              // paste_add_inplace
             if (stg) {
                 stg[(size_t)rr * W + c] = o;

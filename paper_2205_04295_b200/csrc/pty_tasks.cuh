@@ -414,7 +414,7 @@ __device__ __forceinline__ T task_row_inv_update(const cplx<T>* tw, cplx<T>* lin
         const C o = ov[q];
         T den = gamma * peak + (T(1) - gamma) * ppv[q];
         den = den + eps_rel * dmax_o;
-        const C no = o + divr(scale(nrow[c], alpha_o), den);
+        const C no = o + scale(scale(nrow[c], alpha_o), rcp_fast(den));
         orow[c] = o + (no - o);                                // paste_add_inplace
         if (stg) {
             stg[(size_t)r * W + c] = o;
@@ -506,22 +506,23 @@ __device__ __forceinline__ T task_row_inv_update_staged(const cplx<T>* tw, cplx<
             T dp = beta * omax + (T(1) - beta) * norm2(o);
             dp = dp + eps_rel * dmax_p;
             const T idp = rcp_fast(dp);
+            const OMul<T> om(o);
             C numer{T(0), T(0)};
             T npp = T(0);
 #pragma unroll
             for (int m = 0; m < MODES; ++m) {
                 const C X = lines[(m * 4 + rr) * LS4 + pad<W>(c)];
-                const C d = scale(X, checker<T>(r, c) * invW2) - pv[m][k] * o;
+                const C d = scale(X, checker<T>(r, c) * invW2) - om.mul(pv[m][k]);
                 numer = numer + mulc(d, pv[m][k]);
                 if (U.update_probe) {
-                    const C np_ = pv[m][k] + scale(mulc(scale(d, alpha_p), o), idp);
+                    const C np_ = pv[m][k] + scale(om.mulconj(scale(d, alpha_p)), idp);
                     probes[m * WW + (size_t)r * W + c] = np_;
                     npp += norm2(np_);
                 }
             }
             T den = gamma * peak + (T(1) - gamma) * ppv[k];
             den = den + eps_rel * dmax_o;
-            const C no = o + divr(scale(numer, alpha_o), den);
+            const C no = o + scale(scale(numer, alpha_o), rcp_fast(den));
             obj[(size_t)(ar + r) * Wc + ac + c] = o + (no - o);          // paste_add_inplace
             if (stg) {
                 stg[(size_t)r * W + c] = o;
