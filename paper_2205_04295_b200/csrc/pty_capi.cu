@@ -313,6 +313,7 @@ int pty_orthogonalize(void* probes, int32_t dtype, int32_t W, int32_t M, void* s
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const long long n = (long long)M * W * W;
     cplx<double>* work = nullptr;
+    keep_pool_memory();
     if (cudaMallocAsync(&work, n * sizeof(cplx<double>), st) != cudaSuccess) return PTY_ERR_CUDA;
     int rc = with_dtype(dtype, [&](auto t) {
         using T = decltype(t);
@@ -374,6 +375,7 @@ int pty_batch_finalize(const double* err_part, int32_t n_visits, int32_t W, doub
     outs.p[0] = err_out;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     double* vs = nullptr;
+    keep_pool_memory();
     if (cudaMallocAsync(&vs, (size_t)n_visits * 3 * sizeof(double), st) != cudaSuccess) return PTY_ERR_CUDA;
     err_visit_kernel<<<n_visits, 256, 0, st>>>(err_part, W, vs);
     err_slot_kernel<<<1, 256, 0, st>>>(vs, n_visits, 1, outs);

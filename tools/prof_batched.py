@@ -21,5 +21,6 @@ for b in batches:
         a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(); pk.sweep(st, ds, cfg); e.record(); torch.cuda.synchronize()
         ts.append(a.elapsed_time(e))
+    print("sweeps", [round(x, 2) for x in ts])
     ms = min(ts)
     print(f"N={n} b={b}: {ms:.2f} ms/sweep  {n/ms*1e3:,.0f} pos/s  roofline {n/ms*1e3*bench.B_POS/6548.5e9:.1%}  err={st.error_trace[-1]:.4f}", flush=True)
