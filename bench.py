@@ -72,20 +72,28 @@ def make_dataset(seed=1):
 
 # ------------------------------------------------------------- clocks ----
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks/throttle reasons sampled during the timed region.
+
+    nvidia-smi is started before the warm-up (its start-up alone can outlast
+    a short timed region); every sample is stamped on arrival and the summary
+    keeps the samples between mark_start() and mark_end() (plus one polling
+    interval), falling back to the samples nearest the region if none landed
+    inside it."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    PERIOD_MS = 50
 
     def __init__(self, index):
         self.index = index
         self.proc = None
-        self.lines = []
+        self.lines = []          # (host time, csv line)
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", str(self.PERIOD_MS)],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -95,7 +103,18 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.monotonic(), line.strip()))
+
+    def mark_start(self):
+        self.t0 = time.monotonic()
+
+    def mark_end(self):
+        self.t1 = time.monotonic()
+        # make sure at least two samples exist after the region started
+        deadline = self.t1 + 2.0
+        while self.proc is not None and time.monotonic() < deadline and \
+                sum(1 for t, _ in self.lines if t >= self.t0) < 2:
+            time.sleep(0.02)
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -106,9 +125,13 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        lines = self.lines
+        if self.t0 is not None and self.t1 is not None:
+            inside = [(t, ln) for t, ln in lines if self.t0 <= t <= self.t1 + self.PERIOD_MS / 1e3]
+            lines = inside or sorted(lines, key=lambda x: min(abs(x[0] - self.t0), abs(x[0] - self.t1)))[:2]
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for _, ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 6:
                 continue
@@ -156,12 +179,13 @@ def gpu_arm(args, rank, world):
     # ---- value: R replicas resident in HBM, device-timed sweeps
     states = [fresh(r) for r in range(R)]
     dsets = [ds] * R
-    for _ in range(args.warmup):
-        run_states(states, dsets, cfg)
-    torch.cuda.synchronize()
-    step_ms, kern_ms = [], []
-    launches0 = _native.launch_count()
     with ClockSampler(dev.index) as clocks:
+        for _ in range(args.warmup):
+            run_states(states, dsets, cfg)
+        torch.cuda.synchronize()
+        step_ms, kern_ms = [], []
+        launches0 = _native.launch_count()
+        clocks.mark_start()
         for _ in range(args.steps):
             flush_l2(flush)
             if world > 1:
@@ -175,6 +199,7 @@ def gpu_arm(args, rank, world):
             torch.cuda.synchronize()
             step_ms.append(e0.elapsed_time(e1))
             kern_ms.append(k0.elapsed_time(k1))
+        clocks.mark_end()
     launches = _native.launch_count() - launches0
     total_ms = sum(step_ms)
     if world > 1:
