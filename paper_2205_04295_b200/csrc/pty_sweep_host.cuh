@@ -43,7 +43,7 @@ inline SweepLayout carve_sweep(void* ws, int W, int M, int N, int S) {
 }
 
 // few slots (latency): the tile kernel; many slots (throughput): line tasks.
-inline int tiles_max_slots() { return env_int("PTY_SWEEP_TILES_MAX", 8); }
+inline int tiles_max_slots() { return env_int("PTY_SWEEP_TILES_MAX", 4); }   // measured crossover: lines win from 5 slots
 
 template <typename T>
 inline size_t sweep_workspace(int W, int M, int N, int S) {
