@@ -110,6 +110,29 @@ __device__ __forceinline__ unsigned long long gtimer_t() {
 
 // max over n partials, loaded by warp 0 in parallel and broadcast through
 // shared memory.  Every thread of the CTA must call it.
+// Two maxima in one pass (both partial arrays loaded together: one L2 round
+// trip and one pair of barriers instead of two).  cell: 2 shared slots.
+template <typename T>
+__device__ __forceinline__ void t_cta_max2_of(const T* p, const T* q, int n, T* cell, T& a, T& b) {
+    if (threadIdx.x < 32) {
+        T ma = T(0), mb = T(0);
+        for (int i = threadIdx.x; i < n; i += 32) {
+            ma = fmax(ma, p[i]);
+            mb = fmax(mb, q[i]);
+        }
+        ma = warp_max(ma);
+        mb = warp_max(mb);
+        if (threadIdx.x == 0) {
+            cell[0] = ma;
+            cell[1] = mb;
+        }
+    }
+    __syncthreads();
+    a = cell[0];
+    b = cell[1];
+    __syncthreads();
+}
+
 template <typename T>
 __device__ __forceinline__ T t_cta_max_of(const T* p, int n, T* cell) {
     if (threadIdx.x < 32) {
@@ -326,8 +349,9 @@ struct SweepCta {
         const SlotDev& sl = P.slot[s];
         if (s_dead[s]) continue;
         const int j = s_j[s];
-        const T peak = t_cta_max_of(peak_part + ((size_t)(step & 1) * S + s) * P.nRT, P.nRT, cellT);
-        const T omax = t_cta_max_of(omax_part + (size_t)s * P.nRT, P.nRT, cellT);
+        T peak, omax;
+        t_cta_max2_of(peak_part + ((size_t)(step & 1) * S + s) * P.nRT, omax_part + (size_t)s * P.nRT, P.nRT, cellT,
+                      peak, omax);
         if (peak == T(0)) {                      // engine.py:132-134
             if (tid == 0) atomicOr(sl.status, PTY_ERR_PROBE_ZERO);
             continue;
