@@ -183,3 +183,27 @@ def test_criterion_4_two_mode_recovery(gpu):
             pk.sweep(state, ds, cfg)
         errs[mode_count] = _translation_aligned_object_error(state, ds)
     assert errs[2] / errs[1] <= 0.5, errs
+
+
+def test_criterion_5_registration_accuracy(gpu):
+    """test_acceptance.py:216-242: 500 random subpixel shifts registered with
+    raw weighting at kappa = 50 -- here as ONE batched launch
+    (register_batch) -- max per-axis error < 2/kappa; integer rolls exact."""
+    from scipy.ndimage import gaussian_filter
+    kappa = 50
+    rng = np.random.default_rng(12)
+    base = gaussian_filter(rng.standard_normal((64, 64)), sigma=2.0)
+    shifts = [rng.uniform(-3, 3, 2) for _ in range(500)]
+    fy = np.fft.fftfreq(64)[:, None]
+    fx = np.fft.fftfreq(64)[None, :]
+    fb = np.fft.fft2(base)
+    movs = np.stack([np.fft.ifft2(fb * np.exp(-2j * np.pi * (fy * dy + fx * dx))).real for dx, dy in shifts])
+    refs = np.broadcast_to(base, movs.shape).copy()
+    dy, dx, peak, ok = pk.register_batch(refs, movs, "raw", kappa)
+    dy, dx = dy.cpu().numpy(), dx.cpu().numpy()
+    true = np.array(shifts)
+    worst = max(np.abs(dy + true[:, 1]).max(), np.abs(dx + true[:, 0]).max())
+    assert worst < 2.0 / kappa, worst
+    for s in [(0, 0), (3, -5), (-7, 2)]:
+        est = pk.register(base, np.roll(base, s, axis=(0, 1)), weighting="raw", upsample=1)
+        assert (est.dy, est.dx) == (-float(s[0]), -float(s[1]))
