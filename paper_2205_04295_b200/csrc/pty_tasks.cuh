@@ -244,19 +244,25 @@ __device__ __forceinline__ void task_col_mod(const cplx<T>* tw, cplx<T>* xch, in
     constexpr int A = Shape<W>::A, B = Shape<W>::B;
     const size_t WW = (size_t)W * W;
     const T invW2 = T(1) / (T(W) * T(W));
-    T tmax = T(0);
-#pragma unroll
-    for (int i = 0; i < W / B; ++i) tmax = fmax(tmax, tmax_pos[b + i * B]);
-    tmax = group_max<B>(tmax);
-    const T eps = eps_rel * fmax(tmax, real_limits<T>::tiny());
     const T* It = It_pos + (size_t)kc * W;
     const T* tt = totT_pos + (size_t)kc * W;
+    // the column maxima, I and total of this column: one round trip
+    T tmax = T(0), Ia[A], ta[A];
+#pragma unroll
+    for (int i = 0; i < W / B; ++i) tmax = fmax(tmax, tmax_pos[b + i * B]);
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+        Ia[a] = It[B * a + b];
+        ta[a] = tt[B * a + b];
+    }
+    tmax = group_max<B>(tmax);
+    const T eps = eps_rel * fmax(tmax, real_limits<T>::tiny());
     T sc[A], after[A];
     double en = 0.0, ed = 0.0;
 #pragma unroll
     for (int a = 0; a < A; ++a) {
         const int u = B * a + b;
-        const T Iv = It[u], tv = tt[u];
+        const T Iv = Ia[a], tv = ta[a];
         const T sI = sqrt_fast(Iv);
         sc[a] = modulus_scale(sI, tv + eps);
         const T d = sqrt_fast(tv) - sI;
@@ -284,8 +290,7 @@ __device__ __forceinline__ void task_col_mod(const cplx<T>* tw, cplx<T>* xch, in
     if (track) {
 #pragma unroll
         for (int a = 0; a < A; ++a) {
-            const int u = B * a + b;
-            const T Iv = It[u], tv = tt[u];
+            const T Iv = Ia[a], tv = ta[a];
             if (tv > T(1e-3) * tmax) worst = fmax(worst, fabs(after[a] - Iv) / fmax(Iv, real_limits<T>::tiny()));
         }
     }
