@@ -47,6 +47,9 @@ struct SweepDev {
     int resident;                 // P2 -> P3 column lines stay in shared memory (<= 1 column task per group)
     int p4_staged;                // P4: all modes' lines staged in shared memory, element-linear epilogue
     int p1_staged;                // P1: one task per row quad for all modes (needs p4_staged's shared memory)
+    int slot_local;               // every phase's tasks of slot s live on CTAs [s*cps, (s+1)*cps): per-slot barriers
+    int cps;                      // CTAs per slot (slot_local)
+    unsigned int* slot_bar;       // [nslots][32] per-slot barrier counters (slot_local)
     // workspace
     unsigned int* barrier;
     int* anchors;                 // [nslots][N][2]
@@ -195,9 +198,34 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
     T* red4_p4 = acc_base + (size_t)2 * NTEAM * 4 * RS + team * 4;
 
     GridBarrier bar{P.barrier, 0u};
+    // slot-local mode: after phase 0 a CTA only ever waits for the other CTAs
+    // of its own slot (all of a slot's data -- scratch, canvas, probes,
+    // partials -- is touched only by them), so slots drift independently and
+    // a CTA waiting on its slot's barrier leaves the SM to the other slot's CTA
+    bool local = false;
+    unsigned int* my_bar = nullptr;
+    unsigned int my_target = 0u;
     auto phase_sync = [&]() {
-        if constexpr (CL) cluster_sync();
-        else bar.sync();
+        if constexpr (CL) {
+            cluster_sync();
+        } else {
+            if (local) {
+                __syncthreads();
+                my_target += (unsigned)P.cps;
+                if (threadIdx.x == 0) {
+                    unsigned int one = 1u, seen;
+                    asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(seen) : "l"(my_bar), "r"(one) : "memory");
+                    while (true) {
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(my_bar) : "memory");
+                        if ((int)(seen - my_target) >= 0) break;
+                        __nanosleep(20);
+                    }
+                }
+                __syncthreads();
+            } else {
+                bar.sync();
+            }
+        }
     };
     load_twiddles<T, W>(tw, reinterpret_cast<const C*>(P.twiddles));
 
@@ -229,6 +257,14 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
         if (tid == 0) peak_part[(size_t)s * nq + rq] = pk;
     }
     phase_sync();
+    if constexpr (!CL) {
+        if (P.slot_local) {
+            const int my_slot = (int)blockIdx.x / P.cps;
+            if (my_slot >= S) return;                          // idle CTA: no task in any phase
+            local = true;
+            my_bar = P.slot_bar + 32 * my_slot;
+        }
+    }
 
     auto stamp = [&](int step, int k) {
         if (P.timeline && step < P.timeline_steps) {

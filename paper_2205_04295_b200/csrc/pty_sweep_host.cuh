@@ -21,6 +21,7 @@ struct SweepLayout {
     double* err_part;
     double* visit_sum;
     void* ppg;
+    unsigned int* slot_bar;
     size_t bytes;
 };
 
@@ -38,6 +39,7 @@ inline SweepLayout carve_sweep(void* ws, int W, int M, int N, int S) {
     L.err_part = c.take<double>((size_t)S * N * W * 3 * sizeof(double));
     L.visit_sum = c.take<double>((size_t)S * N * 3 * sizeof(double));
     L.ppg = c.take<void>((size_t)S * W * W * sizeof(T));
+    L.slot_bar = c.take<unsigned int>((size_t)S * 32 * sizeof(unsigned int));
     L.bytes = c.off;
     return L;
 }
@@ -155,6 +157,14 @@ int run_sweep_lines(const PtySweepArgs* a, cudaStream_t st) {
         if (want > 0) per_sm = std::min(per_sm, want);
         grid = sm_count() * per_sm;
         if ((long)S * W > (long)grid * NGRP) P.resident = 0;   // more than one column task per group
+        // slot-local barriers: one round of tasks in every phase and the same
+        // CTA range per slot for row-quad tasks (teams) and column tasks (groups)
+        const int cps_rows = (W / 4) / NTEAM4, cps_cols = W / NGRP;
+        P.cps = cps_rows;
+        P.slot_local = (env_int("PTY_SLOT_BARRIER", 1) && P.p1_staged && P.p4_staged && P.resident &&
+                        cps_rows == cps_cols && cps_rows >= 1 && (long)S * cps_rows <= grid &&
+                        (W / 4) % NTEAM4 == 0 && W % NGRP == 0) ? 1 : 0;
+        P.slot_bar = L.slot_bar;
     }
 
     // debug timeline (PTY_TIMELINE=<steps>): per-CTA phase completion stamps
@@ -166,6 +176,7 @@ int run_sweep_lines(const PtySweepArgs* a, cudaStream_t st) {
         P.timeline_steps = tl_steps;
     }
     if (cudaMemsetAsync(L.barrier, 0, sizeof(unsigned int), st) != cudaSuccess) return PTY_ERR_CUDA;
+    if (cudaMemsetAsync(L.slot_bar, 0, (size_t)S * 32 * sizeof(unsigned int), st) != cudaSuccess) return PTY_ERR_CUDA;
     if (cudaMemsetAsync(L.err_part, 0, (size_t)S * N * W * 3 * sizeof(double), st) != cudaSuccess)
         return PTY_ERR_CUDA;
     cudaError_t e;
