@@ -121,3 +121,23 @@ def test_reference_datasets_are_readable(tmp_path):
     pk.write_dataset(tmp_path / "r", ds)
     back = pk.read_dataset(tmp_path / "r")
     np.testing.assert_array_equal(back.patterns, g["patterns"].astype(np.float64))
+
+
+def test_integration_stub_structs_match_the_abi():
+    """INTEGRATION.md's maintainer stub declares the same PtySlot / PtySweepArgs
+    layout as the package's binding (field names, offsets, sizes)."""
+    import ctypes as C
+    import re
+    from pathlib import Path
+    from paper_2205_04295_b200 import _native
+    text = (Path(__file__).resolve().parents[1] / "INTEGRATION.md").read_text()
+    code = re.search(r"```python\n# ptychokit/_b200.py.*?\n(.*?)```", text, re.S).group(1)
+    code = code.split("lib.pty_sweep.argtypes")[0].replace('lib = C.CDLL("libptycho_b200.so")', "")
+    ns = {}
+    exec(code, ns)
+    for name in ("PtySlot", "PtySweepArgs"):
+        a, b = ns[name], getattr(_native, name)
+        assert C.sizeof(a) == C.sizeof(b), name
+        assert [f[0] for f in a._fields_] == [f[0] for f in b._fields_], name
+        for f in a._fields_:
+            assert getattr(a, f[0]).offset == getattr(b, f[0]).offset, (name, f[0])
