@@ -495,12 +495,10 @@ __device__ __forceinline__ T task_row_inv_update_staged(const cplx<T>* tw, cplx<
 #pragma unroll 1
     for (int h = 0; h < NE; h += CH) {
         C ov[CH], pv[MODES][CH];
-        T ppv[CH];
 #pragma unroll
         for (int k = 0; k < CH; ++k) {
             const int e = tl + (h + k) * TEAM, rr = e / W, c = e % W, r = 4 * rq + rr;
             ov[k] = obj[(size_t)(ar + r) * Wc + ac + c];
-            ppv[k] = ppg[(size_t)r * W + c];
 #pragma unroll
             for (int m = 0; m < MODES; ++m) pv[m][k] = probes[m * WW + (size_t)r * W + c];
         }
@@ -525,7 +523,11 @@ __device__ __forceinline__ T task_row_inv_update_staged(const cplx<T>* tw, cplx<
                     npp += norm2(np_);
                 }
             }
-            T den = gamma * peak + (T(1) - gamma) * ppv[k];
+            // sum_m |P_m|^2 of this visit's probes, in mode order (engine.py:129)
+            T ppk = T(0);
+#pragma unroll
+            for (int m = 0; m < MODES; ++m) ppk += norm2(pv[m][k]);
+            T den = gamma * peak + (T(1) - gamma) * ppk;
             den = den + eps_rel * dmax_o;
             const C no = o + scale(scale(numer, alpha_o), rcp_fast(den));
             obj[(size_t)(ar + r) * Wc + ac + c] = o + (no - o);          // paste_add_inplace
@@ -533,12 +535,7 @@ __device__ __forceinline__ T task_row_inv_update_staged(const cplx<T>* tw, cplx<
                 stg[(size_t)r * W + c] = o;
                 stg[WW + (size_t)r * W + c] = no;
             }
-            if (U.update_probe) {
-                ppg[(size_t)r * W + c] = npp;
-                pk = fmax(pk, npp);
-            } else {
-                pk = fmax(pk, ppv[k]);
-            }
+            pk = fmax(pk, U.update_probe ? npp : ppk);
         }
     }
     pk = group_max<B>(pk);
