@@ -349,18 +349,7 @@ struct SweepCta {
         const SlotDev& sl = P.slot[s];
         if (s_dead[s]) continue;
         const int j = s_j[s];
-        T peak, omax;
-        t_cta_max2_of(peak_part + ((size_t)(step & 1) * S + s) * P.nRT, omax_part + (size_t)s * P.nRT, P.nRT, cellT,
-                      peak, omax);
-        if (peak == T(0)) {                      // engine.py:132-134
-            if (tid == 0) atomicOr(sl.status, PTY_ERR_PROBE_ZERO);
-            continue;
-        }
-        if (P.update_probe && omax == T(0)) {    // engine.py:145-147
-            if (tid == 0) atomicOr(sl.status, PTY_ERR_OBJECT_ZERO);
-            continue;
-        }
-        const int ar = s_ar[s], ac = s_ac[s];
+        const int ar = s_ar[s], ac = s_ac[s];   // the row loads below do not need the maxima: issued first
         {   // obj / probe rows of the update: into L1 while the inverse DFTs run
             const bool l1 = (size_t)P.TR * (M + 1) * W * sizeof(C) <= 16 * 1024;
             for (int r = 0; r < P.TR; ++r) {
@@ -390,6 +379,17 @@ struct SweepCta {
                     if (i < nel) tile[(size_t)(i / W) * LS + pad<W>(i % W)] = v[u];
                 }
             });
+        }
+        T peak, omax;
+        t_cta_max2_of(peak_part + ((size_t)(step & 1) * S + s) * P.nRT, omax_part + (size_t)s * P.nRT, P.nRT, cellT,
+                      peak, omax);
+        if (peak == T(0)) {                      // engine.py:132-134
+            if (tid == 0) atomicOr(sl.status, PTY_ERR_PROBE_ZERO);
+            continue;
+        }
+        if (P.update_probe && omax == T(0)) {    // engine.py:145-147
+            if (tid == 0) atomicOr(sl.status, PTY_ERR_OBJECT_ZERO);
+            continue;
         }
         __syncthreads();
         lines_fft<T, W, true>(tile, P.TR * M, LS, tw);
