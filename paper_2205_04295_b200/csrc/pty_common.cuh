@@ -152,6 +152,26 @@ template <typename T> __device__ __forceinline__ T warp_sum(T v) {
 
 // Block-wide max / sum; `red` is >= 32 entries of shared scratch.  Every
 // thread returns the result.  Must be called by all threads of the block.
+// The three per-visit error terms (sum, sum, max) reduced over the block in
+// one pass: two barriers instead of six.  red: >= 48 doubles, blocks of at
+// most 16 warps.  Every thread returns the results.
+template <typename T> __device__ void block_err3(double& a, double& b, T& c, double* red) {
+    a = warp_sum(a);
+    b = warp_sum(b);
+    c = warp_max(c);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (lane == 0) {
+        red[wid] = a;
+        red[16 + wid] = b;
+        red[32 + wid] = (double)c;
+    }
+    __syncthreads();
+    a = warp_sum(lane < nw ? red[lane] : 0.0);
+    b = warp_sum(lane < nw ? red[16 + lane] : 0.0);
+    c = (T)warp_max(lane < nw ? red[32 + lane] : 0.0);
+}
+
 template <typename T> __device__ T block_max(T v, T* red) {
     v = warp_max(v);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;

@@ -323,9 +323,7 @@ struct SweepCta {
         __syncthreads();
         lines_fft<T, W, true>(my, M * P.TC, LS, tw);
         __syncthreads();
-        enum_ = block_sum(enum_, reinterpret_cast<double*>(red));
-        eden = block_sum(eden, reinterpret_cast<double*>(red));
-        worst = block_max(worst, red);
+        block_err3(enum_, eden, worst, reinterpret_cast<double*>(red));
         if (tid == 0) {
             double* e = P.err_part + (((size_t)s * N + step) * P.nCT + ct) * 3;
             e[0] = enum_;
