@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -40,6 +41,9 @@ sys.path.insert(0, str(ROOT))
 W, M, GRID, STEP_PX, RADIUS = 256, 3, (20, 20), 32.0, 60.0
 POWERS = (0.8, 0.1, 0.1)
 B_POS = W * W * (20 + 16 * M)        # algorithmic bytes per position
+# algorithmic FFT flops per position: 2M 2-D transforms of W x W at 5 N log2 N
+# ("algorithmic flops per position"); 31.5 MFLOP at 256^2 x 3
+FFT_FLOP_POS = 2 * M * 5 * W * W * int(math.log2(W * W))
 METRIC = "diffraction positions/sec per rPIE iteration at 256x256x3 modes; % HBM roofline"
 WORKLOAD = ("config 2: simulated 20x20 scan (400 positions), 256x256 patterns, 3 mixed-state "
             "probe modes, rPIE alpha=0.9 beta=gamma=0.5, Fraunhofer, shuffled order")
@@ -51,6 +55,15 @@ def peaks():
         d = json.loads(p.read_text())
         return float(d["hbm_gbs"]), "measured"
     return 6650.0, "fallback"
+
+
+def fp32_peak_tflops():
+    """FP32 FMA peak, derived (not measured): 148 SMs x 128 lanes x 2 flop x max SM clock."""
+    mhz = 1965.0
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        mhz = float(json.loads(p.read_text()).get("sm_max_mhz", mhz))
+    return 148 * 128 * 2 * mhz * 1e6 / 1e12
 
 
 def solver_config(precision="fp32"):
@@ -213,6 +226,7 @@ def gpu_arm(args, rank, world):
     kernel_s = kern_total / 1e3 / args.steps                 # per sweep launch (R*n positions)
     hbm, peak_kind = peaks()
     achieved = R * n * B_POS / kernel_s / 1e9
+    fft_tflops = R * n * FFT_FLOP_POS / kernel_s / 1e12
     traffic = None
     tp = ROOT / "profiles" / "sweep_traffic.json"
     if tp.exists():
@@ -244,7 +258,7 @@ def gpu_arm(args, rank, world):
     # D2H of its result inside the timed region, every step
     e2e = e2e_arm(args, states, ds, cfg, dev, world)
     return dict(value=value, ms_per_step=total_ms / args.steps, kernel_ms=kern_total / args.steps,
-                achieved=achieved, hbm=hbm, peak_kind=peak_kind, traffic=traffic, clocks=clocks.summary(),
+                achieved=achieved, fft_tflops=fft_tflops, hbm=hbm, peak_kind=peak_kind, traffic=traffic, clocks=clocks.summary(),
                 launches=launches, single=single, e2e=e2e, n=n)
 
 
@@ -570,6 +584,10 @@ def main():
                          "kernel": "pty::sweep_kernel<float,256> (persistent cooperative sweep)",
                          "bytes_per_position": B_POS, "peak_kind": res["peak_kind"],
                          "kernel_ms_per_step": res["kernel_ms"]},
+            "fft": {"bound": "fp32", "achieved": res["fft_tflops"], "peak": fp32_peak_tflops(),
+                    "unit": "TFLOP/s", "frac": res["fft_tflops"] / fp32_peak_tflops(),
+                    "flops_per_position": FFT_FLOP_POS, "convention": "5 N log2 N per 2-D transform, 2M transforms per visit",
+                    "peak_kind": "derived 148 SM x 128 FMA lanes x 2 x sm_max_mhz"},
             "cpu_baseline": cpu,
             "e2e": res["e2e"],
             "gpu_launches": res["launches"],
