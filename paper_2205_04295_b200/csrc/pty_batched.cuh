@@ -8,8 +8,10 @@
 // per SM so load latency of one CTA overlaps the DFTs of another.
 //   bk_probe_power : pp = sum_m |P_m|^2 map and its max (engine.py:129-132)
 //   bk_rows_fwd    : exit waves, row DFTs -> scratch[k]; max|o_k|^2 partials
-//   bk_cols_fwd    : column DFTs, Psi -> scratch[k]; max(total) partials
-//   bk_cols_mod    : modulus constraint, error terms, inverse column DFTs
+//   bk_cols_fwd    : column DFTs -> total^T and max(total) partials (Psi is
+//                    not written back: one scratch write pass saved)
+//   bk_cols_mod    : column DFTs recomputed, modulus constraint, error terms,
+//                    inverse column DFTs
 //   bk_rows_inv    : inverse row DFTs -> psi'; object numerator per position
 //                    (onum[k]); probe numerator/denominator summed over a fixed
 //                    group of positions per CTA (deterministic)
@@ -143,8 +145,10 @@ __global__ void __launch_bounds__(kLineThreads) bk_rows_fwd(const __grid_constan
     }
 }
 
-// K2: column DFTs of every mode, Psi written back in place, total^T and
-// max(total) partial per column (engine.py:114-117).  Group task (k, kc).
+// K2: column DFTs of every mode, total^T and max(total) partial per column
+// (engine.py:114-117); Psi stays on chip (K3 recomputes it: the grid-wide
+// max(total) of the position must be known before the modulus scale, and a
+// second DFT costs less than a scratch write + read).  Group task (k, kc).
 template <typename T, int W>
 __global__ void __launch_bounds__(kLineThreads) bk_cols_fwd(const __grid_constant__ BatchDev P) {
     using C = cplx<T>;
@@ -164,12 +168,12 @@ __global__ void __launch_bounds__(kLineThreads) bk_cols_fwd(const __grid_constan
     T* totT = reinterpret_cast<T*>(P.totT);
     for (int task = blockIdx.x * NG + grp; task < P.b * W; task += gridDim.x * NG) {
         const int k = task / W, kc = task % W;
-        const T tm = task_col_fwd<T, W>(tw, xch, b, gmask, scratch + (size_t)k * M * WW, M, kc, totT + (size_t)k * WW);
+        const T tm = task_col_fwd<T, W, false, false>(tw, xch, b, gmask, scratch + (size_t)k * M * WW, M, kc, totT + (size_t)k * WW);
         if (b == 0) reinterpret_cast<T*>(P.tmax_part)[(size_t)k * W + kc] = tm;
     }
 }
 
-// K3: modulus constraint scale = sqrt(I)/sqrt(total + eps) (engine.py:117-118),
+// K3: forward column DFTs recomputed from the row-DFT output, modulus constraint scale = sqrt(I)/sqrt(total + eps) (engine.py:117-118),
 // error terms (engine.py:198-214), inverse column DFTs.  Group task (k, kc).
 template <typename T, int W>
 __global__ void __launch_bounds__(kLineThreads) bk_cols_mod(const __grid_constant__ BatchDev P) {
@@ -191,7 +195,7 @@ __global__ void __launch_bounds__(kLineThreads) bk_cols_mod(const __grid_constan
     for (int task = blockIdx.x * NG + grp; task < P.b * W; task += gridDim.x * NG) {
         const int k = task / W, kc = task % W, j = P.batch[k];
         C* stg = P.sense == PTY_SENSE_XCORR_B ? reinterpret_cast<C*>(P.stage) + (size_t)j * 2 * WW : nullptr;
-        task_col_mod<T, W>(tw, xch, b, gmask, scratch + (size_t)k * M * WW, M, kc, totT + (size_t)k * WW,
+        task_col_mod<T, W, false, true>(tw, xch, b, gmask, scratch + (size_t)k * M * WW, M, kc, totT + (size_t)k * WW,
                            reinterpret_cast<const T*>(P.tmax_part) + (size_t)k * W,
                            reinterpret_cast<const T*>(P.patternsT) + (size_t)j * WW, T(P.eps_rel), P.track_mod, stg,
                            P.err_part + ((size_t)(P.visit0 + k) * W + kc) * 3);

@@ -189,8 +189,9 @@ __device__ __forceinline__ T task_row_fwd_staged(const cplx<T>* tw, cplx<T>* lin
 
 // Column pass, group task (column kc) of one position: forward column DFTs of
 // every mode written back in place (Psi), total = sum_m |Psi_m|^2 (engine.py:
-// 114-116) stored transposed; returns the column's max(total).
-template <typename T, int W, bool RES = false>
+// 114-116) stored transposed; returns the column's max(total).  STORE = false
+// keeps Psi off HBM (the batched column pass 2 recomputes it, REFWD below).
+template <typename T, int W, bool RES = false, bool STORE = true>
 __device__ __forceinline__ T task_col_fwd(const cplx<T>* tw, cplx<T>* xch, int b, unsigned gmask, cplx<T>* pos, int M,
                                           int kc, T* totT_pos, cplx<T>* res = nullptr) {
     using C = cplx<T>;
@@ -214,7 +215,7 @@ __device__ __forceinline__ T task_col_fwd(const cplx<T>* tw, cplx<T>* xch, int b
             group_fft<T, W, false>(
                 xch, tw, b, gmask, [&](int n, int) { return line[n]; },
                 [&](int u, int slot, C v) {
-                    line[u] = v;
+                    if constexpr (STORE) line[u] = v;
                     tot[slot] += norm2(v) * invW2;
                 });
         }
@@ -235,7 +236,10 @@ __device__ __forceinline__ T task_col_fwd(const cplx<T>* tw, cplx<T>* xch, int b
 // tmax_pos: the position's W column maxima; It: the transposed pattern.
 // stg (XCORR_B sensor planes, row-major total and I) may be null.
 // Writes err[0..2] = (sum (sqrt(total)-sqrt(I))^2, sum I, worst modulus error).
-template <typename T, int W, bool RES = false>
+// REFWD: `pos` holds the row-DFT output, not Psi; each mode's forward column
+// DFT is recomputed into the group's exchange line (same code as
+// task_col_fwd) instead of being read back from HBM.
+template <typename T, int W, bool RES = false, bool REFWD = false>
 __device__ __forceinline__ void task_col_mod(const cplx<T>* tw, cplx<T>* xch, int b, unsigned gmask, cplx<T>* pos,
                                              int M, int kc, const T* totT_pos, const T* tmax_pos, const T* It_pos,
                                              T eps_rel, int track, cplx<T>* stg, double* err,
@@ -277,10 +281,15 @@ __device__ __forceinline__ void task_col_mod(const cplx<T>* tw, cplx<T>* xch, in
     for (int m = 0; m < M; ++m) {
         C* line = pos + m * WW + (size_t)kc * W;
         C* rl = RES ? res + m * xch_size<W>() : xch;      // resident Psi_m from P2
+        if constexpr (REFWD) {
+            group_fft<T, W, false>(
+                xch, tw, b, gmask, [&](int n, int) { return line[n]; }, [&](int u, int, C v) { xch[pad<W>(u)] = v; });
+            __syncwarp(gmask);
+        }
         group_fft<T, W, true>(
             rl, tw, b, gmask,
             [&](int n, int a) {
-                const C v = scale(RES ? rl[pad<W>(n)] : line[n], sc[a]);
+                const C v = scale((RES || REFWD) ? rl[pad<W>(n)] : line[n], sc[a]);
                 after[a] += norm2(v) * invW2;
                 return v;
             },
