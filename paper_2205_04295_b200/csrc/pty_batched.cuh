@@ -346,20 +346,37 @@ __global__ void __launch_bounds__(256) bk_obj_gather(const __grid_constant__ Bat
     T den[PX];
 #pragma unroll
     for (int q = 0; q < PX; ++q) { num[q] = C{T(0), T(0)}; den[q] = T(0); }
+    // the next covering position's anchors are fetched while this one's
+    // numerators load (one dependent L2 round trip per position instead of two)
+    int k = list[0], ar = P.anchors[2 * k], ac = P.anchors[2 * k + 1];
     for (int t = 0; t < total; ++t) {
-        const int k = list[t];
-        const int ar = P.anchors[2 * k], ac = P.anchors[2 * k + 1];
+        int kn = k, arn = ar, acn = ac;
+        if (t + 1 < total) {
+            kn = list[t + 1];
+            arn = P.anchors[2 * kn];
+            acn = P.anchors[2 * kn + 1];
+        }
 #pragma unroll
         for (int q = 0; q < PX; ++q) {
             const int p = threadIdx.x + q * 256, R = R0 + p / kObjTile, Cc = C0 + p % kObjTile;
             const int r = R - ar, c = Cc - ac;
             if (R < P.H && Cc < P.Wc && r >= 0 && r < W && c >= 0 && c < W) {
-                C s = onum[(size_t)k * P.M * WW + (size_t)r * W + c];
-                for (int m = 1; m < P.M; ++m) s = s + onum[((size_t)k * P.M + m) * WW + (size_t)r * W + c];
+                const C* src = onum + (size_t)k * P.M * WW + (size_t)r * W + c;
+                C v[kMaxBatchModes];                          // every mode's load in flight at once
+#pragma unroll
+                for (int m = 0; m < kMaxBatchModes; ++m)
+                    if (m < P.M) v[m] = src[(size_t)m * WW];
+                C s = v[0];
+#pragma unroll
+                for (int m = 1; m < kMaxBatchModes; ++m)
+                    if (m < P.M) s = s + v[m];               // mode order, as before
                 num[q] = num[q] + s;
                 den[q] += gamma * peak + (T(1) - gamma) * pp[(size_t)r * W + c];
             }
         }
+        k = kn;
+        ar = arn;
+        ac = acn;
     }
 #pragma unroll
     for (int q = 0; q < PX; ++q) {
