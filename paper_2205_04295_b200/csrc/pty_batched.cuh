@@ -242,8 +242,13 @@ __global__ void bk_rows_inv(const __grid_constant__ BatchDev P) {
         const C* prow = probes + m * WW + (size_t)r * W;
 #pragma unroll
         for (int q = 0; q < A; ++q) pv[q] = prow[b + B * (q / B) + A * (q % B)];
+        int arn = g < P.b ? P.anchors[2 * g] : 0, acn = g < P.b ? P.anchors[2 * g + 1] : 0;
         for (int k = g; k < P.b; k += P.G) {
-            const int ar = P.anchors[2 * k], ac = P.anchors[2 * k + 1];
+            const int ar = arn, ac = acn;                      // the next position's anchors load during this one
+            if (k + P.G < P.b) {
+                arn = P.anchors[2 * (k + P.G)];
+                acn = P.anchors[2 * (k + P.G) + 1];
+            }
             const T* op = reinterpret_cast<const T*>(P.omax_part) + (size_t)k * nq;
             T omax = T(0);
             for (int q = b; q < nq; q += B) omax = fmax(omax, op[q]);
@@ -312,22 +317,34 @@ __global__ void __launch_bounds__(256) bk_obj_gather(const __grid_constant__ Bat
     if (threadIdx.x == 0) total = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int base = 0; base < P.b; base += blockDim.x) {
-        const int k = base + threadIdx.x;
-        bool cov = false;
-        if (k < P.b) {
-            const int ar = P.anchors[2 * k], ac = P.anchors[2 * k + 1];
-            cov = ar < R0 + kObjTile && ar + W > R0 && ac < C0 + kObjTile && ac + W > C0;
+    constexpr int LR = 8;                                     // list rounds whose anchor loads fly together
+    for (int base0 = 0; base0 < P.b; base0 += LR * blockDim.x) {
+        bool covr[LR];
+#pragma unroll
+        for (int u = 0; u < LR; ++u) {
+            const int k = base0 + u * blockDim.x + threadIdx.x;
+            covr[u] = false;
+            if (k < P.b) {
+                const int ar = P.anchors[2 * k], ac = P.anchors[2 * k + 1];
+                covr[u] = ar < R0 + kObjTile && ar + W > R0 && ac < C0 + kObjTile && ac + W > C0;
+            }
         }
-        const unsigned bal = __ballot_sync(0xffffffffu, cov);
-        if (lane == 0) wcount[wid] = __popc(bal);
-        __syncthreads();
-        int off = total;
-        for (int w = 0; w < wid; ++w) off += wcount[w];
-        if (cov) list[off + __popc(bal & ((1u << lane) - 1u))] = k;
-        __syncthreads();
-        if (threadIdx.x == 0) for (int w = 0; w < (int)(blockDim.x >> 5); ++w) total += wcount[w];
-        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < LR; ++u) {
+            const int base = base0 + u * blockDim.x;
+            if (base >= P.b) break;                           // block-uniform
+            const int k = base + threadIdx.x;
+            const bool cov = covr[u];
+            const unsigned bal = __ballot_sync(0xffffffffu, cov);
+            if (lane == 0) wcount[wid] = __popc(bal);
+            __syncthreads();
+            int off = total;
+            for (int w = 0; w < wid; ++w) off += wcount[w];
+            if (cov) list[off + __popc(bal & ((1u << lane) - 1u))] = k;
+            __syncthreads();
+            if (threadIdx.x == 0) for (int w = 0; w < (int)(blockDim.x >> 5); ++w) total += wcount[w];
+            __syncthreads();
+        }
     }
     if (total == 0) return;
     const T* pp = reinterpret_cast<const T*>(P.pp);
