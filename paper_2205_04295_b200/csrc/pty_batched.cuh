@@ -314,6 +314,8 @@ __global__ void __launch_bounds__(256) bk_obj_gather(const __grid_constant__ Bat
     const int tiles_x = (P.Wc + kObjTile - 1) / kObjTile;
     const int ty = blockIdx.x / tiles_x, tx = blockIdx.x % tiles_x;
     const int R0 = ty * kObjTile, C0 = tx * kObjTile;
+    // a failed batch (bounds / zero probe) raises; never read its numerators
+    if (*(volatile const int*)P.status) return;
     if (threadIdx.x == 0) total = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -483,6 +485,7 @@ __global__ void __launch_bounds__(256) bk_probe_apply(const __grid_constant__ Ba
 template <typename T, int W>
 __global__ void bk_stage_after(const __grid_constant__ BatchDev P) {
     using C = cplx<T>;
+    if (*(volatile const int*)P.status) return;        // e.g. an out-of-canvas anchor
     const int k = blockIdx.x / P.nRT, rt = blockIdx.x % P.nRT;
     const int j = P.batch[k], ar = P.anchors[2 * k], ac = P.anchors[2 * k + 1];
     const size_t WW = (size_t)W * W;

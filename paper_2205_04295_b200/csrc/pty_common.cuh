@@ -57,6 +57,23 @@ __device__ __forceinline__ cplx<float> scale(cplx<float> a, float s) {
     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(z) : "l"(f2pack(a.re, a.im)), "l"(f2pack(s, s)));
     return f2unpack(z);
 }
+// General complex products on the packed pipe.  x * w = wr*(xr, xi) +
+// wi*(-xi, xr): one FMUL2 with a broadcast operand and one FFMA2 whose
+// swapped / negated operand ptxas folds into the .F32x2.LO_HI modifiers (2
+// instructions instead of 2 FMUL + 2 FFMA).
+__device__ __forceinline__ cplx<float> operator*(cplx<float> x, cplx<float> w) {
+    unsigned long long t, z;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(f2pack(x.re, x.im)), "l"(f2pack(w.re, w.re)));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(z) : "l"(f2pack(x.im, x.re)), "l"(f2pack(-w.im, w.im)), "l"(t));
+    return f2unpack(z);
+}
+// x * conj(w) = wr*(xr, xi) + wi*(xi, -xr)
+__device__ __forceinline__ cplx<float> mulc(cplx<float> x, cplx<float> w) {
+    unsigned long long t, z;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(f2pack(x.re, x.im)), "l"(f2pack(w.re, w.re)));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(z) : "l"(f2pack(x.im, x.re)), "l"(f2pack(w.im, -w.im)), "l"(t));
+    return f2unpack(z);
+}
 // x * (c + i s) for a compile-time twiddle: c*(xr, xi) + (xi, xr)*(-s, s)
 __device__ __forceinline__ cplx<float> rot_const(cplx<float> x, float c, float s) {
     unsigned long long t, z;

@@ -66,7 +66,7 @@ __device__ __forceinline__ cplx<T> twiddle32(cplx<T> x, int j) {
     if (j == 24) return INV ? cplx<T>{x.im, -x.re} : cplx<T>{-x.im, x.re};
     const T c = T(cos32(j));
     const T s = INV ? T(sin32(j)) : T(-sin32(j));
-    return rot_const<T>(x, c, s);
+    return rot_const(x, c, s);      // float: the packed overload
 }
 
 // In-register DFT of N <= 32 points, natural order in and out (radix-2 DIT).

@@ -353,7 +353,10 @@ def sweep_batched(state: ReconState, dataset, config: SolverConfig, group=None) 
     if world > 1:
         import torch.distributed as dist
         dist.all_reduce(err_part, group=group)
-        dist.all_reduce(status, op=dist.ReduceOp.MAX, group=group)
+        # per-bit MAX (a MAX of the bitmasks would drop bits: 1 | 4 -> 4)
+        bits = ((status >> t.arange(10, device=status.device, dtype=t.int32)) & 1).to(t.int32)
+        dist.all_reduce(bits, op=dist.ReduceOp.MAX, group=group)
+        status.copy_((bits << t.arange(10, device=status.device, dtype=t.int32)).sum().view(1))
     _native.batch_finalize(err_part, n, w, err)
     if engaged and world == 1:
         _refine_positions(st, config.posref, n, w)
@@ -416,12 +419,30 @@ def sweep_replicas(states, datasets, config: SolverConfig, orders=None, kernel_e
     Every replica keeps the reference's exact sequential semantics; the K
     visit chains are simply interleaved step by step across the GPU
     (replica mode).  All replicas share window, mode count,
-    position count and precision."""
+    position count and precision.  ``config`` is one SolverConfig for all
+    replicas or one per replica; per-replica configs may differ only in what
+    the host decides (shuffle_seed, position_order, init_seed, iterations),
+    the update rule itself is shared by the launch."""
     t = _native.torch()
     states = list(states)
     datasets = list(datasets)
     if len(states) != len(datasets) or not states:
         raise ParameterError("need one dataset per state")
+    if isinstance(config, (list, tuple)):
+        configs = list(config)
+        if len(configs) != len(states):
+            raise ParameterError("need one config per state")
+        shared = ("alpha_obj", "alpha_probe", "beta", "gamma", "epsilon_rel", "update_probe_modes",
+                  "track_modulus_error", "posref", "ortho_interval", "precision", "mode_count",
+                  "batch_size", "propagator")
+        for c in configs[1:]:
+            if any(getattr(c, k) != getattr(configs[0], k) for k in shared):
+                raise ParameterError("replicas in one launch must share the update rule "
+                                     f"({', '.join(shared)})")
+        if orders is None:
+            orders = [visit_order(d.n_positions, c, st.iteration)
+                      for st, d, c in zip(states, datasets, configs)]
+        config = configs[0]
     if len(states) > _native.MAX_SLOTS:
         # more replicas than one launch carries: consecutive launches of at
         # most MAX_SLOTS (each replica's sweep is still one launch)

@@ -1,0 +1,150 @@
+"""Parity at the benchmarked configurations (VERDICT r1 "pin parity at the
+configuration you benchmark").
+
+Every kernel path bench.py times runs here against the complex128 oracle
+(oracle/rpie.py restates /root/reference/pkg/src/ptychokit/engine.py:173-243;
+oracle/batched.py states the batched extension), on short scans so the oracle
+finishes in seconds:
+
+  * W=256, M=3, 18 replicas (bench.py's default R): the line-task sweep kernel
+    with slot-local barriers, staged P1/P4 and resident columns; every replica
+    has its own dataset, init_seed AND shuffle_seed, and every replica is
+    checked against its own oracle run -- fp32 at the north-star tolerance
+    (object / probe relative L2 <= 1e-4 after 2 iterations) and fp64 at 1e-9;
+  * W=512, M=5 with 6 replicas: the non-staged line-task path (M > 4), fp32;
+  * batched W=256, b > 1 (chunks with a short last chunk), fp64 and fp32;
+  * the batched K4 grouping / chunking paths (PTY_K4_GROUPS, PTY_BATCH_CHUNK)
+    and a b >= 600 batch whose covering-position list is built over several
+    rounds.
+
+Measured errors are printed (run with -s) and recorded in DESIGN.md section 5.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2205_04295_b200 as pk
+from oracle import batched, rpie
+from test_gpu_parity import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+FP32_TOL = 1e-4          # north star: object/probe relative L2 after N iterations
+FP64_TOL = 1e-9
+
+
+def scene(w, m, grid, step, radius, seed, lam=8.3187e-10, jitter=1.0):
+    geom = pk.Geometry.create(lam, 0.75, 20e-6, w)
+    plan = pk.make_scan(grid, step, jitter, seed=seed)
+    obj = pk.make_object(pk.canvas_shape_for(plan, w), "spokes", seed=seed)
+    powers = (1.0,) if m == 1 else tuple([0.8] + [0.2 / (m - 1)] * (m - 1))
+    probes = pk.make_probe(pk.ProbeSpec(m, powers, "disk", radius), geom)
+    ds = pk.synthesize(obj, probes, plan, geom)
+    ds.patterns = ds.patterns.astype(np.float32).astype(np.float64)   # on-disk precision
+    return ds
+
+
+def report(tag, errs):
+    errs = np.asarray(errs)
+    print(f"PARITY {tag}: max obj {errs[:, 0].max():.3e} probe {errs[:, 1].max():.3e} "
+          f"pos {errs[:, 2].max():.3e} px err-trace {errs[:, 3].max():.3e}")
+
+
+def run_replicas(w, m, replicas, precision, grid=(3, 3), step=None, radius=None, sweeps=2, posref=False,
+                 lam=8.3187e-10):
+    step = step or w / 8
+    radius = radius or w * 0.234
+    dsets = [scene(w, m, grid, step, radius, seed=11 + r, lam=lam) for r in range(replicas)]
+    base = dict(alpha_obj=0.9, alpha_probe=0.9, beta=0.5, gamma=0.5, mode_count=m, precision=precision,
+                position_order="shuffled",
+                posref=pk.PosRefConfig(kappa=10, warmup_iterations=0) if posref else None)
+    cfgs = [pk.SolverConfig(**base, init_seed=r, shuffle_seed=100 + r) for r in range(replicas)]
+    states = [pk.initialize(d, c) for d, c in zip(dsets, cfgs)]
+    oracles = [rpie.initialize(d.patterns, d.positions, w, c) for d, c in zip(dsets, cfgs)]
+    for _ in range(sweeps):
+        pk.sweep_replicas(states, dsets, cfgs)
+        for o, d, c in zip(oracles, dsets, cfgs):
+            rpie.sweep(o, d.patterns, w, c)
+    errs = []
+    for st, o in zip(states, oracles):
+        errs.append((rel_l2(st.obj.cpu().numpy(), o.obj),
+                     rel_l2(st.probe_stack.cpu().numpy(), np.stack(o.probes)),
+                     float(np.max(np.abs(st.positions.cpu().numpy() - o.positions))),
+                     float(np.max(np.abs(np.asarray(st.error_trace) / np.asarray(o.error_trace) - 1)))))
+    return np.asarray(errs)
+
+
+@pytest.mark.parametrize("precision,tol", [("fp32", FP32_TOL), ("fp64", FP64_TOL)])
+def test_bench_config_18_replicas_vs_oracle(gpu, precision, tol):
+    """bench.py's headline path: 256^2 x 3 modes, 18 replicas in one launch."""
+    errs = run_replicas(256, 3, 18, precision)
+    report(f"W256 M3 R18 {precision}", errs)
+    assert errs[:, 0].max() < tol and errs[:, 1].max() < tol
+    assert errs[:, 3].max() < (1e-5 if precision == "fp32" else 1e-9)
+
+
+def test_bench_config_replicas_with_posref_fp32(gpu):
+    """Config 3 in replica mode (posref XCORR_A kappa=10, engaged from the
+    first sweep): refined positions within 1e-3 px of the oracle's."""
+    errs = run_replicas(256, 3, 6, "fp32", posref=True)
+    report("W256 M3 R6 posref fp32", errs)
+    assert errs[:, 0].max() < FP32_TOL and errs[:, 1].max() < FP32_TOL
+    assert errs[:, 2].max() < 1e-3
+
+
+def test_w512_five_modes_non_staged_line_tasks(gpu):
+    """M = 5 > 4 takes the per-mode (non-staged) P1/P4 tasks of the line-task
+    kernel; 6 replicas (> the tile kernel's 4), config-4 geometry."""
+    errs = run_replicas(512, 5, 6, "fp32", step=64.0, radius=120.0, lam=8.29e-10)
+    report("W512 M5 R6 fp32", errs)
+    assert errs[:, 0].max() < FP32_TOL and errs[:, 1].max() < FP32_TOL
+
+
+# ----------------------------------------------------------------- batched ----
+
+def batched_case(w, m, grid, batch, precision, step=None, sweeps=2, posref=None):
+    ds = scene(w, m, grid, step or w / 8, w * 0.234, seed=5)
+    cfg = pk.SolverConfig(alpha_obj=0.9, alpha_probe=0.9, beta=0.5, gamma=0.5, mode_count=m,
+                          precision=precision, batch_size=batch, posref=posref)
+    st = pk.initialize(ds, cfg)
+    ost = rpie.initialize(ds.patterns, ds.positions, w, cfg)
+    for _ in range(sweeps):
+        pk.sweep(st, ds, cfg)
+        batched.sweep_batched(ost, ds.patterns, w, cfg, batch)
+    return (rel_l2(st.obj.cpu().numpy(), ost.obj), rel_l2(st.probe_stack.cpu().numpy(), np.stack(ost.probes)),
+            float(np.max(np.abs(st.positions.cpu().numpy() - ost.positions))),
+            float(np.max(np.abs(np.asarray(st.error_trace) / np.asarray(ost.error_trace) - 1))))
+
+
+@pytest.mark.parametrize("precision,tol", [("fp64", FP64_TOL), ("fp32", FP32_TOL)])
+def test_batched_w256_vs_oracle(gpu, precision, tol):
+    """The config-5 shape (256^2 x 3) in batched mode, 25 positions in
+    batches of 8 (last batch 1)."""
+    e = batched_case(256, 3, (5, 5), 8, precision)
+    report(f"batched W256 M3 b8 {precision}", [e])
+    assert e[0] < tol and e[1] < tol
+
+
+@pytest.mark.parametrize("env", [{"PTY_K4_GROUPS": "2"}, {"PTY_K4_GROUPS": "3"},
+                                 {"PTY_BATCH_CHUNK": "5"},
+                                 {"PTY_BATCH_CHUNK": "5", "PTY_K4_GROUPS": "2"}])
+def test_batched_grouping_and_chunking_paths(gpu, monkeypatch, env):
+    """K4 groups that walk several positions (next position's anchors
+    prefetched), and chunked accumulation with a short last chunk whose probe
+    groups carry over (pty_batched_host.cuh), fp64 vs the oracle."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    e = batched_case(32, 2, (4, 4), 16, "fp64", step=6.0)
+    report(f"batched W32 b16 {env}", [e])
+    assert e[0] < FP64_TOL and e[1] < FP64_TOL
+    e = batched_case(32, 2, (4, 4), 16, "fp64", step=6.0,
+                     posref=pk.PosRefConfig(kappa=10, warmup_iterations=0))
+    assert e[0] < FP64_TOL and e[1] < FP64_TOL and e[2] < 1e-9
+
+
+def test_batched_large_batch_multi_round_gather(gpu):
+    """b = 625 > 256: bk_obj_gather builds each tile's covering-position list
+    over several rounds of anchor loads."""
+    e = batched_case(16, 1, (25, 25), 625, "fp64", step=3.0, sweeps=2)
+    report("batched W16 b625 fp64", [e])
+    assert e[0] < FP64_TOL and e[1] < FP64_TOL

@@ -188,7 +188,7 @@ def test_fp64_matches_oracle_at_config1_shape(gpu):
     ulp differences ~10x per sweep (test_chaos_control in test_oracle_cpu.py:
     the oracle against itself with a 1e-15 probe perturbation reaches 8e-3 by
     iteration 20), so at 20 iterations parity is tier Q: error trace within 5%.
-    fp32 (tier S): <= 1e-4 (object) / 1e-3 (probe) after 2 iterations."""
+    fp32: <= 1e-4 (object and probe) after 2 iterations (north star)."""
     geom = pk.Geometry.create(8.3187e-10, 0.75, 20e-6, 128)
     plan = pk.make_scan((10, 10), 16.0, 1.0, seed=1)
     obj = pk.make_object(pk.canvas_shape_for(plan, 128), "spokes", seed=1)
@@ -216,8 +216,10 @@ def test_fp64_matches_oracle_at_config1_shape(gpu):
     for _ in range(2):
         pk.sweep(s32, ds, cfg32)
         rpie.sweep(o64, ds.patterns, 128, cfg32)
-    assert rel_l2(s32.obj.cpu().numpy(), o64.obj) < 1e-4
-    assert rel_l2(s32.probe_stack.cpu().numpy(), np.stack(o64.probes)) < 1e-3
+    e_o = rel_l2(s32.obj.cpu().numpy(), o64.obj)
+    e_p = rel_l2(s32.probe_stack.cpu().numpy(), np.stack(o64.probes))
+    print(f"PARITY config1 fp32 2 sweeps: obj {e_o:.3e} probe {e_p:.3e}")
+    assert e_o < 1e-4 and e_p < 1e-4                     # north star: <= 1e-4 after N iterations
 
 
 def test_fresnel_propagator_matches_explicit_chirp_oracle(gpu):
@@ -274,10 +276,12 @@ def test_config4_shape_512_five_modes_posref(gpu, precision, tol):
     for _ in range(2):
         pk.sweep(st, ds, cfg)
         rpie.sweep(ost, ds.patterns, 512, cfg)
-    assert rel_l2(st.obj.cpu().numpy(), ost.obj) < tol
-    assert rel_l2(st.probe_stack.cpu().numpy(), np.stack(ost.probes)) < 10 * tol
-    np.testing.assert_allclose(st.positions.cpu().numpy(), ost.positions, rtol=0,
-                               atol=1e-9 if precision == "fp64" else 0.11)
+    e_o = rel_l2(st.obj.cpu().numpy(), ost.obj)
+    e_p = rel_l2(st.probe_stack.cpu().numpy(), np.stack(ost.probes))
+    e_x = float(np.max(np.abs(st.positions.cpu().numpy() - ost.positions)))
+    print(f"PARITY config4 {precision}: obj {e_o:.3e} probe {e_p:.3e} pos {e_x:.3e} px")
+    assert e_o < tol and e_p < tol
+    assert e_x < (1e-9 if precision == "fp64" else 1e-3)   # north star: refined positions within 1e-3 px
 
 
 # ------------------------------------------------------------ registration ----
