@@ -20,6 +20,12 @@
  *   pty_init_probes      engine.py:83-95 (mode-1 back-propagation, mode Gram-Schmidt)
  *   pty_orthogonalize    engine.py:153-164 _orthogonalize_modes
  *   pty_check_patterns   engine.py:111-112 (DataError on I < 0), checked once at upload
+ *   pty_magnitude_correct / pty_update_object / pty_update_probe
+ *                        engine.py:104-150 (the per-visit functions, one call each)
+ *   pty_cross_power_spectrum / pty_coarse_argmax / pty_upsampled_idft / pty_argmax_abs
+ *                        registration.py:43-120 (the per-pair pipeline, step by step)
+ *   pty_adam_step / pty_apply_correction
+ *                        posref.py:87-113 (one position)
  *   pty_batch_contrib / pty_batch_apply / pty_batch_finalize
  *                        batched (semi-parallel) extension -- no reference
  *                        counterpart; CPU statement oracle/batched.py
@@ -199,6 +205,65 @@ PTY_API int pty_batch_contrib(const PtyBatchArgs* args, void* stream);
 PTY_API int pty_batch_apply(const PtyBatchArgs* args, void* stream);
 PTY_API int pty_batch_finalize(const double* err_part, int32_t n_visits, int32_t window,
                                double* err_out, void* stream);
+
+/*
+ * Per-visit / per-pair public functions of the reference, one call each
+ * (pty_visit.cu).  All fields are W x W complex (real where noted) device
+ * arrays of the given dtype; `scratch` is device scratch of at least the
+ * *_scratch_bytes() size.  Data-dependent failures are OR-ed into *status.
+ */
+PTY_API int64_t pty_visit_scratch_bytes(int32_t dtype, int32_t window, int32_t modes);
+
+/* engine.py:104-120 magnitude_correct: psi_det[m] = propagate(P_m * o_j),
+ * corrected[m] = propagate(sqrt(I) / sqrt(total + eps) * psi_det[m], backward);
+ * I (real) < 0 anywhere -> PTY_ERR_NEGATIVE_I.  probes/corrected/psi_det: [M][W][W]. */
+PTY_API int pty_magnitude_correct(int32_t dtype, int32_t window, int32_t modes, const void* probes,
+                                  const void* o_j, const void* intensity, double epsilon_rel,
+                                  void* corrected, void* psi_det, int32_t* status,
+                                  void* scratch, int64_t scratch_bytes, void* stream);
+
+/* engine.py:123-137 update_object: out = o_j + alpha numer / denom (zero probe -> PTY_ERR_PROBE_ZERO). */
+PTY_API int pty_update_object(int32_t dtype, int32_t window, int32_t modes, const void* o_j,
+                              const void* probes, const void* corrected, double alpha_obj, double gamma,
+                              double epsilon_rel, void* out, int32_t* status,
+                              void* scratch, int64_t scratch_bytes, void* stream);
+
+/* engine.py:140-150 update_probe (one mode; zero crop -> PTY_ERR_OBJECT_ZERO). */
+PTY_API int pty_update_probe(int32_t dtype, int32_t window, const void* probe, const void* o_j,
+                             const void* corrected, double alpha_probe, double beta, double epsilon_rel,
+                             void* out, int32_t* status, void* scratch, int64_t scratch_bytes, void* stream);
+
+/* registration.py:43-56 cross_power_spectrum of n pairs (work as pty_register_batch):
+ * xps [n][W][W] = F(ref) conj(F(mov)) (uncentered), whitened when weighting = 0
+ * ("phase"); ok[k] = 0 when the spectrum is identically zero. */
+PTY_API int pty_cross_power_spectrum(void* work, const void* ref_real, const void* mov_real,
+                                     int32_t real_inputs, int32_t dtype, int32_t window, int32_t n,
+                                     int32_t weighting, void* xps, int32_t* ok,
+                                     void* scratch, int64_t scratch_bytes, void* stream);
+
+/* registration.py:67-81 coarse_shift, given corr = ifft2(xps) [n][W][W]:
+ * argmax of |corr| over signed lags, ties -> (|dy|+|dx|, dy, dx) smallest. */
+PTY_API int pty_coarse_argmax(const void* corr, int32_t dtype, int32_t window, int32_t n,
+                              double* dy, double* dx, double* peak, void* stream);
+
+/* registration.py:84-96 upsampled_idft: out[n_rows][n_cols] = er @ xps @ ec / W^2 at
+ * fractional lags rows[], cols[] (device float64 arrays). */
+PTY_API int64_t pty_upsampled_idft_scratch_bytes(int32_t dtype, int32_t window, int32_t n_rows);
+PTY_API int pty_upsampled_idft(const void* xps, int32_t dtype, int32_t window, const double* rows,
+                               int32_t n_rows, const double* cols, int32_t n_cols, void* out,
+                               void* scratch, int64_t scratch_bytes, void* stream);
+
+/* np.argmax(np.abs(x)) over n complex values (first maximum) -> *idx, *val. */
+PTY_API int pty_argmax_abs(const void* x, int32_t dtype, int64_t n, int64_t* idx, double* val, void* stream);
+
+/* posref.py:87-99 adam_step for position j; delta[2] = clipped (dx, dy). */
+PTY_API int pty_adam_step(double* m, double* v, int64_t* t, int32_t j, double gx, double gy,
+                          double step_size, double beta1, double beta2, double eps_adam,
+                          double max_correction, double* delta, void* stream);
+
+/* posref.py:102-113 apply_correction for position j; *inside = 1 when no clamping. */
+PTY_API int pty_apply_correction(double* positions, int32_t j, double dx, double dy, double xmin,
+                                 double ymin, double xmax, double ymax, int32_t* inside, void* stream);
 
 #ifdef __cplusplus
 }

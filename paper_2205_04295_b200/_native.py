@@ -96,6 +96,17 @@ def _declare(lib):
         "pty_batch_contrib": (C.c_int, [C.POINTER(PtyBatchArgs), vp]),
         "pty_batch_apply": (C.c_int, [C.POINTER(PtyBatchArgs), vp]),
         "pty_batch_finalize": (C.c_int, [vp, i32, i32, vp, vp]),
+        "pty_visit_scratch_bytes": (i64, [i32, i32, i32]),
+        "pty_magnitude_correct": (C.c_int, [i32, i32, i32, vp, vp, vp, dp, vp, vp, vp, vp, i64, vp]),
+        "pty_update_object": (C.c_int, [i32, i32, i32, vp, vp, vp, dp, dp, dp, vp, vp, vp, i64, vp]),
+        "pty_update_probe": (C.c_int, [i32, i32, vp, vp, vp, dp, dp, dp, vp, vp, vp, i64, vp]),
+        "pty_cross_power_spectrum": (C.c_int, [vp, vp, vp, i32, i32, i32, i32, i32, vp, vp, vp, i64, vp]),
+        "pty_coarse_argmax": (C.c_int, [vp, i32, i32, i32, vp, vp, vp, vp]),
+        "pty_upsampled_idft_scratch_bytes": (i64, [i32, i32, i32]),
+        "pty_upsampled_idft": (C.c_int, [vp, i32, i32, vp, i32, vp, i32, vp, vp, i64, vp]),
+        "pty_argmax_abs": (C.c_int, [vp, i32, i64, vp, vp, vp]),
+        "pty_adam_step": (C.c_int, [vp, vp, vp, i32, dp, dp, dp, dp, dp, dp, dp, vp, vp]),
+        "pty_apply_correction": (C.c_int, [vp, i32, dp, dp, dp, dp, dp, dp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -107,7 +118,10 @@ def _declare(lib):
 EXPORTS = ("pty_abi_version", "pty_launch_count", "pty_barrier_bench", "pty_timeline", "pty_device_info", "pty_sweep_workspace_bytes", "pty_sweep",
            "pty_fft2", "pty_register_batch", "pty_register_scratch_bytes", "pty_adam_apply",
            "pty_init_probes", "pty_orthogonalize", "pty_check_patterns",
-           "pty_batch_workspace_bytes", "pty_batch_contrib", "pty_batch_apply", "pty_batch_finalize")
+           "pty_batch_workspace_bytes", "pty_batch_contrib", "pty_batch_apply", "pty_batch_finalize",
+           "pty_visit_scratch_bytes", "pty_magnitude_correct", "pty_update_object", "pty_update_probe",
+           "pty_cross_power_spectrum", "pty_coarse_argmax", "pty_upsampled_idft_scratch_bytes",
+           "pty_upsampled_idft", "pty_argmax_abs", "pty_adam_step", "pty_apply_correction")
 
 
 def lib_path() -> Path:
@@ -288,3 +302,91 @@ def device_info():
     vals = [C.c_int32() for _ in range(4)]
     check(lib.pty_device_info(*[C.byref(v) for v in vals]), "pty_device_info")
     return tuple(v.value for v in vals)
+
+
+# ----------------------------------------------- per-visit / per-pair calls --
+
+def _visit_scratch(dtype: int, window: int, modes: int):
+    b = int(load(require_device=False).pty_visit_scratch_bytes(dtype, window, modes))
+    if b < 0:
+        raise NativeError("unsupported visit geometry")
+    return workspace(b, "visit")
+
+
+def magnitude_correct(probes, o_j, intensity, eps_rel, corrected, psi_det, status) -> None:
+    """pty_magnitude_correct on device tensors: probes/corrected/psi_det (M, W, W)."""
+    lib = load()
+    m, w = probes.shape[0], probes.shape[-1]
+    d = dtype_code(probes)
+    ws = _visit_scratch(d, w, m)
+    check(lib.pty_magnitude_correct(d, w, m, ptr(probes), ptr(o_j), ptr(intensity), float(eps_rel),
+                                    ptr(corrected), ptr(psi_det), ptr(status), ptr(ws), ws.numel(),
+                                    stream_ptr()), "pty_magnitude_correct")
+
+
+def update_object(o_j, probes, corrected, alpha, gamma, eps_rel, out, status) -> None:
+    lib = load()
+    m, w = probes.shape[0], probes.shape[-1]
+    d = dtype_code(probes)
+    ws = _visit_scratch(d, w, m)
+    check(lib.pty_update_object(d, w, m, ptr(o_j), ptr(probes), ptr(corrected), float(alpha), float(gamma),
+                                float(eps_rel), ptr(out), ptr(status), ptr(ws), ws.numel(), stream_ptr()),
+          "pty_update_object")
+
+
+def update_probe(probe, o_j, corrected, alpha, beta, eps_rel, out, status) -> None:
+    lib = load()
+    w = probe.shape[-1]
+    d = dtype_code(probe)
+    ws = _visit_scratch(d, w, 1)
+    check(lib.pty_update_probe(d, w, ptr(probe), ptr(o_j), ptr(corrected), float(alpha), float(beta),
+                               float(eps_rel), ptr(out), ptr(status), ptr(ws), ws.numel(), stream_ptr()),
+          "pty_update_probe")
+
+
+def cross_power_spectrum(work, window: int, n: int, weighting: int, xps, ok,
+                         ref_real=None, mov_real=None) -> None:
+    lib = load()
+    sb = int(lib.pty_register_scratch_bytes(window, n, 1))
+    ws = workspace(sb, "register")
+    real = ref_real is not None
+    check(lib.pty_cross_power_spectrum(ptr(work), ptr(ref_real), ptr(mov_real), int(real), dtype_code(work),
+                                       window, n, weighting, ptr(xps), ptr(ok), ptr(ws), ws.numel(),
+                                       stream_ptr()), "pty_cross_power_spectrum")
+
+
+def coarse_argmax(corr, dy, dx, peak) -> None:
+    lib = load()
+    w = corr.shape[-1]
+    n = corr.numel() // (w * w)
+    check(lib.pty_coarse_argmax(ptr(corr), dtype_code(corr), w, n, ptr(dy), ptr(dx), ptr(peak), stream_ptr()),
+          "pty_coarse_argmax")
+
+
+def upsampled_idft(xps, rows, cols, out) -> None:
+    lib = load()
+    w = xps.shape[-1]
+    d = dtype_code(xps)
+    nr, nc = rows.numel(), cols.numel()
+    sb = int(lib.pty_upsampled_idft_scratch_bytes(d, w, nr))
+    ws = workspace(sb, "updft")
+    check(lib.pty_upsampled_idft(ptr(xps), d, w, ptr(rows), nr, ptr(cols), nc, ptr(out), ptr(ws), ws.numel(),
+                                 stream_ptr()), "pty_upsampled_idft")
+
+
+def argmax_abs(x, idx, val) -> None:
+    check(load().pty_argmax_abs(ptr(x), dtype_code(x), x.numel(), ptr(idx), ptr(val), stream_ptr()),
+          "pty_argmax_abs")
+
+
+def adam_step(buffers, j: int, gx: float, gy: float, config, delta) -> None:
+    check(load().pty_adam_step(ptr(buffers.m), ptr(buffers.v), ptr(buffers.t), int(j), float(gx), float(gy),
+                               float(config.step_size), float(config.beta1), float(config.beta2),
+                               float(config.eps_adam), float(config.max_correction), ptr(delta), stream_ptr()),
+          "pty_adam_step")
+
+
+def apply_correction(positions, j: int, dx: float, dy: float, bounds, inside) -> None:
+    xmin, ymin, xmax, ymax = (float(b) for b in bounds)
+    check(load().pty_apply_correction(ptr(positions), int(j), float(dx), float(dy), xmin, ymin, xmax, ymax,
+                                      ptr(inside), stream_ptr()), "pty_apply_correction")

@@ -360,7 +360,7 @@ __global__ void reg_finalize(int n, int W, int kappa, int npts, int kRefineRows,
 }
 
 // posref.py:87-113: Adam recurrence in float64 and clamp, one thread per sensed entry
-__global__ void adam_kernel(double* pos, double* m, double* v, long long* t, const double* gx,
+static __global__ void adam_kernel(double* pos, double* m, double* v, long long* t, const double* gx,
                             const double* gy, const int* ok, const int* index, int n, double step,
                             double b1, double b2, double eps, double clip, double xmin, double ymin,
                             double xmax, double ymax) {

@@ -231,6 +231,103 @@ def initialize(dataset, config: SolverConfig) -> ReconState:
                       canvas_origin=(int(origin[0]), int(origin[1])), adam=adam, frame_chirp=chirp)
 
 
+# ------------------------------------------------ per-visit public functions --
+# The reference's visit building blocks (engine.py:104-150), one CUDA call each
+# (pty_magnitude_correct / pty_update_object / pty_update_probe).  numpy inputs
+# run in complex128 and return numpy (the reference's types); torch inputs keep
+# their precision and device and return tensors.  sweep() does not use them: it
+# evaluates the same expressions fused in one launch.
+
+def _is_tensor(a) -> bool:
+    return isinstance(a, _native.torch().Tensor)
+
+
+def _visit_dtype(*arrays):
+    t = _native.torch()
+    for a in arrays:
+        if _is_tensor(a) and a.dtype in (t.complex64, t.float32):
+            return t.complex64, t.float32
+    return t.complex128, t.float64
+
+
+def _stack(fields, cdt):
+    t = _native.torch()
+    if _is_tensor(fields):
+        x = fields
+    else:
+        x = t.stack([f if _is_tensor(f) else t.from_numpy(np.asarray(f, np.complex128)) for f in fields])
+    return x.to(_native.device(), cdt).contiguous()
+
+
+def _field(a, dt):
+    t = _native.torch()
+    x = a if _is_tensor(a) else t.from_numpy(np.ascontiguousarray(np.asarray(a)))
+    return x.to(_native.device(), dt).contiguous()
+
+
+def _check_visit(w, *shapes):
+    from .fields import check_window
+    check_window(w)
+    for sh in shapes:
+        if tuple(sh[-2:]) != (w, w):
+            raise ShapeError(f"visit fields must all be {w}x{w}, got {tuple(sh)}")
+
+
+def magnitude_correct(probes, o_j, i_j, epsilon_rel: float = 1e-12):
+    """engine.py:104-120 -- mixed-state modulus constraint on the GPU.
+
+    Returns (corrected exit waves, original detector waves) as lists of M
+    fields; raises DataError for negative intensities (engine.py:111-112)."""
+    t = _native.torch()
+    cdt, rdt = _visit_dtype(o_j, probes if _is_tensor(probes) else (probes[0] if len(probes) else None))
+    p = _stack(probes, cdt)
+    o = _field(o_j, cdt)
+    i = _field(i_j, rdt)
+    w = o.shape[-1]
+    _check_visit(w, p.shape, o.shape, i.shape)
+    corrected = t.empty_like(p)
+    psi = t.empty_like(p)
+    status = t.zeros(1, dtype=t.int32, device=o.device)
+    _native.magnitude_correct(p, o, i, epsilon_rel, corrected, psi, status)
+    raise_for_status(int(status.item()), "magnitude_correct")
+    if _is_tensor(o_j):
+        return list(corrected.unbind(0)), list(psi.unbind(0))
+    c, d = corrected.cpu().numpy(), psi.cpu().numpy()
+    return [c[k] for k in range(c.shape[0])], [d[k] for k in range(d.shape[0])]
+
+
+def update_object(o_j, probes, psi_corrected, alpha_obj: float, gamma: float,
+                  epsilon_rel: float = 1e-12):
+    """engine.py:123-137 -- rPIE object update of one crop (gamma = 1: ePIE)."""
+    t = _native.torch()
+    cdt, _ = _visit_dtype(o_j, probes if _is_tensor(probes) else (probes[0] if len(probes) else None))
+    o = _field(o_j, cdt)
+    p = _stack(probes, cdt)
+    c = _stack(psi_corrected, cdt)
+    _check_visit(o.shape[-1], o.shape, p.shape, c.shape)
+    out = t.empty_like(o)
+    status = t.zeros(1, dtype=t.int32, device=o.device)
+    _native.update_object(o, p, c, alpha_obj, gamma, epsilon_rel, out, status)
+    raise_for_status(int(status.item()), "update_object")
+    return out if _is_tensor(o_j) else out.cpu().numpy()
+
+
+def update_probe(probe, o_j, psi_corrected, alpha_probe: float, beta: float,
+                 epsilon_rel: float = 1e-12):
+    """engine.py:140-150 -- rPIE probe update of one mode (beta = 1: ePIE)."""
+    t = _native.torch()
+    cdt, _ = _visit_dtype(o_j, probe)
+    p = _field(probe, cdt)
+    o = _field(o_j, cdt)
+    c = _field(psi_corrected, cdt)
+    _check_visit(o.shape[-1], o.shape, p.shape, c.shape)
+    out = t.empty_like(p)
+    status = t.zeros(1, dtype=t.int32, device=o.device)
+    _native.update_probe(p, o, c, alpha_probe, beta, epsilon_rel, out, status)
+    raise_for_status(int(status.item()), "update_probe")
+    return out if _is_tensor(probe) else out.cpu().numpy()
+
+
 def visit_order(n: int, config: SolverConfig, iteration: int) -> np.ndarray:
     """engine.py:177-181."""
     if config.position_order == "shuffled":

@@ -71,3 +71,61 @@ def adam_apply(positions, buffers: AdamBuffers, gx, gy, ok, config: PosRefConfig
     ``positions`` unless ``index`` (int32, device) maps sensed entries to
     position ids."""
     _native.adam_apply(positions, buffers, gx, gy, ok, config, bounds, index)
+
+
+# ------------------------------------------- per-position public functions --
+# posref.py:57-113 one position at a time, on the GPU (the sweep runs the same
+# arithmetic batched over all sensed positions: adam_apply above).
+
+def _sense(reference, moving, weighting: str, kappa: int):
+    """posref.py:57-63 -- (gx, gy, confident); a degenerate spectrum is not confident."""
+    from .errors import DegenerateInputError
+    from .registration import register
+    try:
+        est = register(reference, moving, weighting=weighting, upsample=kappa)
+    except DegenerateInputError:
+        return 0.0, 0.0, False
+    return est.dx, est.dy, True
+
+
+def sense_shift_A(crop_before, crop_after, kappa: int):
+    """posref.py:66-76 -- object crop vs its update, raw weighting."""
+    return _sense(crop_before, crop_after, "raw", kappa)
+
+
+def sense_shift_B(intensity_model, intensity_measured, kappa: int):
+    """posref.py:79-84 -- modelled vs measured intensity (real), raw weighting."""
+    torch = _native.torch()
+
+    def real(a):
+        if isinstance(a, torch.Tensor):
+            return a.real if a.is_complex() else a
+        return np.asarray(a, float)
+    return _sense(real(intensity_model), real(intensity_measured), "raw", kappa)
+
+
+def adam_step(buffers: AdamBuffers, j: int, g, config: PosRefConfig):
+    """posref.py:87-99 -- one Adam update of position j (float64 on the GPU);
+    returns the clipped (dx, dy)."""
+    torch = _native.torch()
+    delta = torch.empty(2, dtype=torch.float64, device=buffers.m.device)
+    gx, gy = (float(v) for v in g)
+    _native.adam_step(buffers, int(j), gx, gy, config, delta)
+    dx, dy = delta.cpu().numpy()
+    return float(dx), float(dy)
+
+
+def apply_correction(positions, j: int, delta, bounds) -> bool:
+    """posref.py:102-113 -- add (dx, dy) to position j and clamp to
+    (xmin, ymin, xmax, ymax); False when the clamp engaged.  ``positions`` is
+    an (N, 2) float64 CUDA tensor (ReconState.positions) or numpy array
+    (updated in place)."""
+    torch = _native.torch()
+    host = not isinstance(positions, torch.Tensor)
+    pos = torch.from_numpy(np.ascontiguousarray(positions, np.float64)).to(_native.device()) if host \
+        else positions
+    inside = torch.empty(1, dtype=torch.int32, device=pos.device)
+    _native.apply_correction(pos, int(j), float(delta[0]), float(delta[1]), bounds, inside)
+    if host:
+        positions[j] = pos[j].cpu().numpy()
+    return bool(inside.item())
