@@ -72,6 +72,14 @@ def solver_config(precision="fp32"):
                            position_order="shuffled", shuffle_seed=0, precision=precision)
 
 
+def replica_configs(cfg, R, rank):
+    """One config per replica: its own init_seed AND shuffle_seed (independent
+    reconstructions, each in exact reference order)."""
+    import paper_2205_04295_b200 as pk
+    return [pk.SolverConfig(**{**cfg.__dict__, "init_seed": rank * 1000 + r, "shuffle_seed": rank * 1000 + r})
+            for r in range(R)]
+
+
 def make_dataset(seed=1):
     import paper_2205_04295_b200 as pk
     geom = pk.Geometry.create(8.3187e-10, 0.75, 20e-6, W)
@@ -167,9 +175,9 @@ def flush_l2(buf):
 
 
 # ------------------------------------------------------------ GPU arm -----
-def run_states(states, datasets, cfg, kernel_events=None):
+def run_states(states, datasets, cfgs, kernel_events=None):
     import paper_2205_04295_b200 as pk
-    pk.sweep_replicas(states, datasets, cfg, kernel_events=kernel_events)
+    pk.sweep_replicas(states, datasets, cfgs, kernel_events=kernel_events)
 
 
 def gpu_arm(args, rank, world):
@@ -180,21 +188,21 @@ def gpu_arm(args, rank, world):
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
     cfg = solver_config(args.precision)
-    ds = make_dataset(seed=1)
-    n = ds.n_positions
     R = args.replicas
+    # every replica is an independent reconstruction of its OWN dataset (scan
+    # jitter, object and synthesised patterns from seed 1 + rank*1000 + r) with
+    # its own init and shuffle seeds, so no two replicas share inputs or order
+    dsets = [make_dataset(seed=1 + rank * 1000 + r) for r in range(R)]
+    cfgs = replica_configs(cfg, R, rank)
+    ds = dsets[0]
+    n = ds.n_positions
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    def fresh(r):
-        c = pk.SolverConfig(**{**cfg.__dict__, "init_seed": rank * 1000 + r})
-        return pk.initialize(ds, c)
-
     # ---- value: R replicas resident in HBM, device-timed sweeps
-    states = [fresh(r) for r in range(R)]
-    dsets = [ds] * R
+    states = [pk.initialize(d, c) for d, c in zip(dsets, cfgs)]
     with ClockSampler(dev.index) as clocks:
         for _ in range(args.warmup):
-            run_states(states, dsets, cfg)
+            run_states(states, dsets, cfgs)
         torch.cuda.synchronize()
         step_ms, kern_ms = [], []
         launches0 = _native.launch_count()
@@ -207,7 +215,7 @@ def gpu_arm(args, rank, world):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            run_states(states, dsets, cfg, kernel_events=(k0, k1))
+            run_states(states, dsets, cfgs, kernel_events=(k0, k1))
             e1.record()
             torch.cuda.synchronize()
             step_ms.append(e0.elapsed_time(e1))
@@ -237,16 +245,16 @@ def gpu_arm(args, rank, world):
     # ---- single reconstruction (R = 1): the reference's own sequential case
     single = None
     if R != 1 and not args.no_single:
-        st1 = [fresh(0)]
+        st1 = [pk.initialize(ds, cfgs[0])]
         for _ in range(2):
-            run_states(st1, [ds], cfg)
+            run_states(st1, [ds], cfgs[:1])
         ms1 = []
         for _ in range(max(3, args.steps // 2)):
             flush_l2(flush)
             torch.cuda.synchronize()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-            run_states(st1, [ds], cfg)
+            run_states(st1, [ds], cfgs[:1])
             b.record()
             torch.cuda.synchronize()
             ms1.append(a.elapsed_time(b))
@@ -256,17 +264,59 @@ def gpu_arm(args, rank, world):
 
     # ---- e2e: the public API on HOST buffers; H2D of the step's inputs and
     # D2H of its result inside the timed region, every step
-    e2e = e2e_arm(args, states, ds, cfg, dev, world)
-    return dict(value=value, ms_per_step=total_ms / args.steps, kernel_ms=kern_total / args.steps,
+    e2e = e2e_arm(args, states, dsets, cfgs, dev, world)
+    fp64 = None
+    if args.precision == "fp32" and not args.no_fp64:
+        fp64 = fp64_leg(args, dsets, dev, world, flush)
+    return dict(fp64=fp64, value=value, ms_per_step=total_ms / args.steps, kernel_ms=kern_total / args.steps,
                 achieved=achieved, fft_tflops=fft_tflops, hbm=hbm, peak_kind=peak_kind, traffic=traffic, clocks=clocks.summary(),
                 launches=launches, single=single, e2e=e2e, n=n)
 
 
-def e2e_arm(args, states, ds, cfg, dev, world):
-    """The public API fed from HOST memory every step: the step's input (the
-    diffraction stack, pinned host float32) is copied to the device and
-    re-laid out (the transposed copy the column passes stream), the R
-    reconstructions sweep it, and the step's result (every replica's error
+def fp64_leg(args, dsets, dev, world, flush):
+    """The same workload (same R distinct datasets and seeds) through the
+    complex128 instantiation of the sweep kernel -- the reference's own
+    precision, beside the fp64 reference arm."""
+    import torch
+    import paper_2205_04295_b200 as pk
+    R = len(dsets)
+    cfgs = replica_configs(solver_config("fp64"), R, int(os.environ.get("RANK", 0)))
+    states = [pk.initialize(d, c) for d, c in zip(dsets, cfgs)]
+    for _ in range(2):
+        run_states(states, dsets, cfgs)
+    ms = []
+    for _ in range(max(2, args.steps // 3)):
+        flush_l2(flush)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        run_states(states, dsets, cfgs)
+        b.record()
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    total = sum(ms)
+    if world > 1:
+        t = torch.tensor([total], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total = t.item()
+    per = total / len(ms)
+    n = dsets[0].n_positions
+    hbm, _ = peaks()
+    v = R * n * world / (per / 1e3)
+    del states
+    torch.cuda.empty_cache()
+    return {"dtype": "c128", "replicas": R, "value": v, "unit": "positions/s", "ms_per_step": per,
+            "roofline_frac_c64_bytes": v * B_POS / (hbm * 1e9 * world),
+            "note": "complex128 kernels (2x the bytes of the c64 B_pos the roofline uses)"}
+
+
+def e2e_arm(args, states, dsets, cfgs, dev, world):
+    """The public API fed from HOST memory every step: every replica's input
+    (its own diffraction stack, pinned host float32) is copied to the device
+    and re-laid out (the transposed copy the column passes stream), the R
+    reconstructions sweep, and the step's result (every replica's error
     metric and status word) is read back -- all inside the timed region, which
     spans the K steps as one region (the first step's copy is not overlapped).
     The reconstruction state stays resident on the device between steps, as a
@@ -274,16 +324,16 @@ def e2e_arm(args, states, ds, cfg, dev, world):
     import torch
     import paper_2205_04295_b200 as pk
     R = len(states)
-    host_pat = torch.from_numpy(np.ascontiguousarray(ds.patterns, np.float32)).pin_memory()
-    dsx = pk.PtychoDataset(patterns=ds.patterns, positions=ds.positions, geometry=ds.geometry)
-    dev_pat = pk.engine.device_patterns(dsx, torch.float32)
-    dev_pat_t = pk.engine.device_patterns_t(dsx, torch.float32)
+    hosts = [torch.from_numpy(np.ascontiguousarray(d.patterns, np.float32)).pin_memory() for d in dsets]
+    dxs = [pk.PtychoDataset(patterns=d.patterns, positions=d.positions, geometry=d.geometry) for d in dsets]
+    dev_pat = [pk.engine.device_patterns(x, torch.float32) for x in dxs]
+    dev_pat_t = [pk.engine.device_patterns_t(x, torch.float32) for x in dxs]
     # the H2D of step i+1 runs on a copy stream (copy engines, no SMs) while
-    # step i sweeps: two pinned-to-device staging buffers, event-ordered; each
-    # step then moves its staged input into the dataset's device buffers
+    # step i sweeps: two pinned-to-device staging sets, event-ordered; each
+    # step then moves its staged inputs into the datasets' device buffers
     main = torch.cuda.current_stream()
     cstream = torch.cuda.Stream()
-    stage = [torch.empty_like(dev_pat) for _ in range(2)]
+    stage = [[torch.empty_like(p) for p in dev_pat] for _ in range(2)]
     copied = [torch.cuda.Event() for _ in range(2)]
     consumed = [torch.cuda.Event() for _ in range(2)]
     used = [False, False]
@@ -293,7 +343,8 @@ def e2e_arm(args, states, ds, cfg, dev, world):
         if used[slot]:
             cstream.wait_event(consumed[slot])
         with torch.cuda.stream(cstream):
-            stage[slot].copy_(host_pat, non_blocking=True)        # H2D: step i's input
+            for st_, h in zip(stage[slot], hosts):
+                st_.copy_(h, non_blocking=True)                      # H2D: step i's inputs
             copied[slot].record(cstream)
 
     def run_steps(n):
@@ -303,11 +354,12 @@ def e2e_arm(args, states, ds, cfg, dev, world):
             main.wait_event(copied[slot])
             if i + 1 < n:
                 issue_copy(i + 1)
-            dev_pat.copy_(stage[slot])
-            dev_pat_t.copy_(stage[slot].transpose(1, 2))          # device re-layout
+            for r in range(R):
+                dev_pat[r].copy_(stage[slot][r])
+                dev_pat_t[r].copy_(stage[slot][r].transpose(1, 2))  # device re-layout
             consumed[slot].record(main)
             used[slot] = True
-            pk.sweep_replicas(states, [dsx] * R, cfg)              # ends with the D2H of the metric
+            pk.sweep_replicas(states, dxs, cfgs)                     # ends with the D2H of the metric
 
     run_steps(args.warmup)
     torch.cuda.synchronize()
@@ -316,17 +368,17 @@ def e2e_arm(args, states, ds, cfg, dev, world):
     run_steps(args.steps)
     b.record()
     torch.cuda.synchronize()
-    ms = [a.elapsed_time(b)]
-    h2d = host_pat.numel() * 4
+    total = a.elapsed_time(b)
+    h2d = sum(h.numel() * 4 for h in hosts)
     d2h = R * (3 * 8 + 4)                                          # error triple + status per replica
-    total = sum(ms)
     if world > 1:
         t = torch.tensor([total], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total = t.item()
-    value = R * ds.n_positions * args.steps * world / (total / 1e3)
+    value = R * dsets[0].n_positions * args.steps * world / (total / 1e3)
     return {"value": value, "unit": "positions/s", "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h)}
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": total / args.steps,
+            "inputs": f"{R} distinct diffraction stacks uploaded every step"}
 
 
 # ------------------------------------------- other named configs (1, 3, 4) ----
@@ -335,9 +387,9 @@ CONFIGS = {
     "config1": dict(W=128, M=1, grid=(10, 10), step=16.0, radius=30.0, powers=(1.0,), lam=8.3187e-10,
                     posref=False, propagator="farfield"),
     "config3": dict(W=256, M=3, grid=(20, 20), step=32.0, radius=60.0, powers=(0.8, 0.1, 0.1), lam=8.3187e-10,
-                    posref=True, propagator="farfield"),
+                    posref=True, propagator="farfield", replicas=18, distinct_data=True),
     "config4": dict(W=512, M=5, grid=(40, 40), step=64.0, radius=120.0, powers=(0.8, 0.05, 0.05, 0.05, 0.05),
-                    lam=8.29e-10, posref=True, propagator="fresnel"),
+                    lam=8.29e-10, posref=True, propagator="fresnel", replicas=6, distinct_data=False),
 }
 
 
@@ -385,6 +437,44 @@ def configs_leg(args):
                          "iterations_per_s": 1e3 / ms, "ms_per_iteration": ms,
                          "roofline_frac": n / (ms / 1e3) * bpos / (hbm * 1e9),
                          "error_trace_last": st.error_trace[-1]}
+            R = c.get("replicas", 0)
+            if R > 1 and not args.no_config_replicas:
+                # replica mode: R independent reconstructions in one launch per
+                # sweep (own init and shuffle seeds; config 3: own datasets too)
+                del st
+                torch.cuda.empty_cache()
+                if c.get("distinct_data"):
+                    dsets = [ds]
+                    for r in range(1, R):
+                        pl = pk.make_scan(c["grid"], c["step"], 1.0, seed=1 + r)
+                        ob = pk.make_object(pk.canvas_shape_for(pl, w), "spokes", seed=1 + r)
+                        d = pk.synthesize(ob, probes, pl, geom, noise="none", seed=1 + r,
+                                          propagator=c["propagator"])
+                        d.patterns = d.patterns.astype(np.float32)
+                        if c["posref"]:
+                            d.positions = d.positions + np.random.default_rng(42 + r).uniform(-2, 2, d.positions.shape)
+                        dsets.append(d)
+                    shared = "own dataset, init and shuffle seed per replica"
+                else:
+                    dsets = [ds] * R
+                    shared = "one dataset, own init and shuffle seed per replica"
+                cfgs = replica_configs(cfg, R, 0)
+                sts = [pk.initialize(d, cc) for d, cc in zip(dsets, cfgs)]
+                for _ in range(2):
+                    pk.sweep_replicas(sts, dsets, cfgs)
+                rsteps = 2 if w >= 512 else 4
+                torch.cuda.synchronize()
+                a.record()
+                for _ in range(rsteps):
+                    pk.sweep_replicas(sts, dsets, cfgs)
+                e.record()
+                torch.cuda.synchronize()
+                rms = a.elapsed_time(e) / rsteps
+                out[name]["replicas"] = {"replicas": R, "data": shared, "positions_per_s": R * n / (rms / 1e3),
+                                         "ms_per_iteration": rms,
+                                         "roofline_frac": R * n / (rms / 1e3) * bpos / (hbm * 1e9),
+                                         "error_trace_last_max": max(x.error_trace[-1] for x in sts)}
+                del sts
         except Exception as exc:                      # report, never lose the main line
             out[name] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
         finally:
@@ -545,6 +635,8 @@ def main():
     ap.add_argument("--no-single", action="store_true")
     ap.add_argument("--no-batched", action="store_true")
     ap.add_argument("--no-configs", action="store_true")
+    ap.add_argument("--no-config-replicas", action="store_true")
+    ap.add_argument("--no-fp64", action="store_true")
     ap.add_argument("--batch", type=int, default=1600)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
@@ -605,6 +697,7 @@ def main():
             "dtype": "c64" if args.precision == "fp32" else "c128", "data": "synthetic",
             "config": {"workload": WORKLOAD, "window": W, "modes": M, "positions": res["n"],
                        "replicas_per_gpu": args.replicas, "precision": args.precision,
+                       "replica_data": "every replica its own dataset (seed 1 + rank*1000 + r), init_seed and shuffle_seed",
                        "parallelism": f"replicas x{args.replicas} per GPU x{world} GPUs",
                        "l2": "256 MiB buffer rewritten between timed steps"},
             "roofline": {"bound": "hbm", "achieved": res["achieved"], "peak": res["hbm"], "unit": "GB/s",
@@ -621,6 +714,7 @@ def main():
             "gpu_launches": res["launches"],
             "clocks": res["clocks"],
             "single_reconstruction": res["single"],
+            "fp64": res["fp64"],
             "batched": batched,
             "configs": configs,
             "iterations_per_s": 1e3 / res["ms_per_step"],

@@ -262,14 +262,15 @@ def barrier_bench(iters: int = 10000, ctas: int = 0) -> float:
 
 
 def timeline():
-    """Debug stamps of the last sweep run with PTY_TIMELINE set: (steps, 5, grid) ns."""
+    """Debug stamps of the last sweep run with PTY_TIMELINE set: (steps, 9, grid) ns
+    (0 step start, 2k-1 end of phase k, 2k barrier exit after phase k)."""
     import numpy as np
     lib = load(require_device=False)
     g = C.c_int32()
     n = lib.pty_timeline(None, 0, C.byref(g))
     buf = np.zeros(n, dtype=np.uint64)
     lib.pty_timeline(buf.ctypes.data, n, C.byref(g))
-    return buf.reshape(-1, 5, g.value) if n else buf
+    return buf.reshape(-1, 9, g.value) if n else buf
 
 
 def launch_count() -> int:

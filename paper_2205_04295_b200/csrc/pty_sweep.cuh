@@ -61,7 +61,7 @@ struct SweepDev {
     double* err_part;             // [nslots][N][W][3] per-visit, per-column error terms
     void* ppg;                    // [nslots][W][W] real: sum_m |P_m|^2 of the current probes
     const void* twiddles;         // [W] complex, global
-    unsigned long long* timeline; // debug: [steps][5][gridDim] globaltimer stamps or null
+    unsigned long long* timeline; // debug: [steps][9][gridDim] globaltimer stamps or null
     int timeline_steps;
     SlotDev slot[kMaxSlots];
 };
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
     auto stamp = [&](int step, int k) {
         if (P.timeline && step < P.timeline_steps) {
             __syncthreads();
-            if (tid == 0) P.timeline[((size_t)step * 5 + k) * gridDim.x + blockIdx.x] = gtimer();
+            if (tid == 0) P.timeline[((size_t)step * 9 + k) * gridDim.x + blockIdx.x] = gtimer();
         }
     };
     for (int step = 0; step < N; ++step) {
@@ -332,6 +332,7 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
         }
         stamp(step, 1);
         phase_sync();
+        stamp(step, 2);
         // ------------------------------------------------- P2 cols (forward)
         for (int task = cta * NGRP + grp; task < S * W; task += ncta * NGRP) {
             const int s = s0 + task / W, kc = task % W;
@@ -341,8 +342,9 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
                 : task_col_fwd<T, W, false>(tw, xch, b, gmask, scratch + (size_t)s * M * WW, M, kc, totT + (size_t)s * WW);
             if (b == 0) tmax_part[(size_t)s * W + kc] = tm;
         }
-        stamp(step, 2);
+        stamp(step, 3);
         phase_sync();
+        stamp(step, 4);
         // ---------------------------------------- P3 modulus + cols (inverse)
         for (int task = cta * NGRP + grp; task < S * W; task += ncta * NGRP) {
             const int s = s0 + task / W, kc = task % W;
@@ -359,8 +361,9 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
                 task_col_mod<T, W, false>(tw, xch, b, gmask, scratch + (size_t)s * M * WW, M, kc, totT + (size_t)s * WW,
                                           tmax_part + (size_t)s * W, It, T(P.eps_rel), P.track_mod, stg, ep);
         }
-        stamp(step, 3);
+        stamp(step, 5);
         phase_sync();
+        stamp(step, 6);
         // --------------------------------------- P4 rows (inverse) + update
         for (int task = cta * NTEAM + team; task < S * nq; task += ncta * NTEAM) {
             const int s = s0 + task / nq, rq = task % nq;
@@ -409,8 +412,9 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
             }
             if (tl == 0) peak_part[((size_t)((step + 1) & 1) * P.nslots + s) * nq + rq] = npk;
         }
-        stamp(step, 4);
+        stamp(step, 7);
         phase_sync();
+        stamp(step, 8);
     }
 }
 

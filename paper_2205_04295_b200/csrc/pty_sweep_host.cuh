@@ -171,7 +171,7 @@ int run_sweep_lines(const PtySweepArgs* a, cudaStream_t st) {
     const int tl_steps = std::min(env_int("PTY_TIMELINE", 0), N);
     unsigned long long* tl = nullptr;
     if (tl_steps > 0) {
-        if (cudaMalloc(&tl, (size_t)tl_steps * 5 * grid * sizeof(unsigned long long)) != cudaSuccess) return PTY_ERR_CUDA;
+        if (cudaMalloc(&tl, (size_t)tl_steps * 9 * grid * sizeof(unsigned long long)) != cudaSuccess) return PTY_ERR_CUDA;
         P.timeline = tl;
         P.timeline_steps = tl_steps;
     }
@@ -204,7 +204,7 @@ int run_sweep_lines(const PtySweepArgs* a, cudaStream_t st) {
     err_slot_kernel<<<S, 256, 0, st>>>(L.visit_sum, N, S, outs);
     count(3);
     if (tl) {
-        g_timeline.assign((size_t)tl_steps * 5 * grid, 0ull);
+        g_timeline.assign((size_t)tl_steps * 9 * grid, 0ull);
         cudaMemcpyAsync(g_timeline.data(), tl, g_timeline.size() * sizeof(unsigned long long),
                         cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);

@@ -58,7 +58,7 @@ struct SweepDev {
     void* tmax_part;              // [nslots][nCT] real
     double* err_part;             // [nslots][N][nCT][3] per-visit error partials
     const void* twiddles;         // [W] complex, global
-    unsigned long long* timeline; // debug: [steps][5][gridDim] globaltimer stamps or null
+    unsigned long long* timeline; // debug: [steps][9][gridDim] globaltimer stamps (phase ends at 1,3,5,7) or null
     int timeline_steps;
     SlotDev slot[kMaxSlots];
 };
@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMinCtasPerSm) sweep_kerne
     auto stamp = [&](int step, int k) {
         if (P.timeline && step < P.timeline_steps) {
             __syncthreads();
-            if (tid == 0) P.timeline[((size_t)step * 5 + k) * gridDim.x + blockIdx.x] = gtimer_t();
+            if (tid == 0) P.timeline[((size_t)step * 9 + (k ? 2 * k - 1 : 0)) * gridDim.x + blockIdx.x] = gtimer_t();
         }
     };
     for (int step = 0; step < N; ++step) {
