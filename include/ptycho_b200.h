@@ -12,6 +12,7 @@
  *   pty_sweep            engine.py:173-243  sweep()  (inner loop engine.py:191-233)
  *                          + fields.py:87-107 crop / paste_add_inplace
  *                          + engine.py:104-150 magnitude_correct / update_object / update_probe
+ *   pty_sweep_subpixel   (extension) simulate.py:157-166 extract_view applied to the sweep's crops
  *   pty_fft2             fields.py:71-84 propagate()  (centered=1), and the
  *                          uncentered np.fft.fft2/ifft2 of registration.py:47,71
  *   pty_register_batch   registration.py:43-128 cross_power_spectrum / coarse_shift /
@@ -120,6 +121,13 @@ PTY_API int64_t pty_sweep_workspace_bytes(int32_t dtype, int32_t window, int32_t
 
 /* One full sweep (every position of every slot) as one cooperative kernel. */
 PTY_API int pty_sweep(const PtySweepArgs* args, void* stream);
+
+/* Opt-in subpixel reconstruction gather (extension, no reference counterpart;
+ * SolverConfig.subpixel_gather): the sweep of pty_sweep with every crop shifted
+ * by its position's residual (simulate.py:157-166 applied to reconstruction)
+ * and the object update shifted back before the paste.  Same arguments as
+ * pty_sweep (workspace unused); track_modulus must be 0. */
+PTY_API int pty_sweep_subpixel(const PtySweepArgs* args, void* stream);
 
 /* In-place batched 2D FFT of `batch` W x W complex fields.
  * centered=1: fields.py propagate (fftshift . fft2 . ifftshift, norm="ortho");

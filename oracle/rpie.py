@@ -243,9 +243,22 @@ def sense(pc, o_before, o_after, total, i_j):
     return est.dx, est.dy, True
 
 
+def subpixel_shift(f: np.ndarray, dx: float, dy: float) -> np.ndarray:
+    """fields.py:110-122 -- circular shift by (dy, dx) through a Fourier phase ramp."""
+    h, w = f.shape
+    fy = np.fft.fftfreq(h)[:, None]
+    fx = np.fft.fftfreq(w)[None, :]
+    return np.fft.ifft2(np.fft.fft2(f) * np.exp(-2j * np.pi * (fy * dy + fx * dx)))
+
+
 def sweep(st: OracleState, patterns, window: int, cfg, order=None, chirp=None) -> OracleState:
     """engine.py:173-243 -- one pass over every position, mutating ``st``.
-    ``chirp``: Fresnel quadratic phase (extension; None = the reference)."""
+    ``chirp``: Fresnel quadratic phase (extension; None = the reference).
+    ``cfg.subpixel_gather`` (extension, parity unpinned): the crop is the
+    simulator's extract_view (simulate.py:157-166) -- integer crop shifted by
+    (-rx, -ry) -- and the object update is shifted back by (rx, ry) before the
+    paste; a residual of exactly zero leaves the crop untouched."""
+    subpixel = bool(getattr(cfg, "subpixel_gather", False))
     n = patterns.shape[0]
     if order is None:
         order = visit_order(n, cfg.position_order, cfg.shuffle_seed, st.iteration)
@@ -264,6 +277,11 @@ def sweep(st: OracleState, patterns, window: int, cfg, order=None, chirp=None) -
         if not box_inside(r, c, window, st.obj.shape):
             raise IndexError(f"crop box at ({r},{c}) outside canvas")
         o_j = st.obj[r:r + window, c:c + window].copy()
+        rx = float(st.positions[j, 0]) - ac
+        ry = float(st.positions[j, 1]) - ar
+        shifted = subpixel and (rx != 0.0 or ry != 0.0)
+        if shifted:
+            o_j = subpixel_shift(o_j, -rx, -ry).astype(st.obj.dtype)
         corrected, det, _ = modulus_project(st.probes, o_j, i_j, cfg.epsilon_rel, chirp)
         total = np.zeros(i_j.shape, dtype=rdt)
         for d in det:
@@ -283,7 +301,10 @@ def sweep(st: OracleState, patterns, window: int, cfg, order=None, chirp=None) -
         if cfg.update_probe_modes and cfg.alpha_probe > 0:
             st.probes = [probe_step(p, o_j, cw, cfg.alpha_probe, cfg.beta, cfg.epsilon_rel)
                          for p, cw in zip(st.probes, corrected)]
-        st.obj[r:r + window, c:c + window] += new_o - o_j
+        delta = new_o - o_j
+        if shifted:
+            delta = subpixel_shift(delta, rx, ry).astype(st.obj.dtype)
+        st.obj[r:r + window, c:c + window] += delta
         if engaged:
             gx, gy, ok = sense(pc, o_j, new_o, total, i_j)
             if ok:

@@ -84,6 +84,7 @@ def _declare(lib):
         "pty_device_info": (C.c_int, [C.POINTER(i32)] * 4),
         "pty_sweep_workspace_bytes": (i64, [i32] * 5),
         "pty_sweep": (C.c_int, [C.POINTER(PtySweepArgs), vp]),
+        "pty_sweep_subpixel": (C.c_int, [C.POINTER(PtySweepArgs), vp]),
         "pty_fft2": (C.c_int, [vp, i32, i32, i32, i32, i32, vp]),
         "pty_register_batch": (C.c_int, [vp, vp, vp, i32, i32, i32, i32, i32, i32,
                                          vp, vp, vp, vp, vp, i64, vp]),
@@ -115,7 +116,7 @@ def _declare(lib):
     return lib
 
 
-EXPORTS = ("pty_abi_version", "pty_launch_count", "pty_barrier_bench", "pty_timeline", "pty_device_info", "pty_sweep_workspace_bytes", "pty_sweep",
+EXPORTS = ("pty_abi_version", "pty_launch_count", "pty_barrier_bench", "pty_timeline", "pty_device_info", "pty_sweep_workspace_bytes", "pty_sweep", "pty_sweep_subpixel",
            "pty_fft2", "pty_register_batch", "pty_register_scratch_bytes", "pty_adam_apply",
            "pty_init_probes", "pty_orthogonalize", "pty_check_patterns",
            "pty_batch_workspace_bytes", "pty_batch_contrib", "pty_batch_apply", "pty_batch_finalize",
@@ -219,6 +220,11 @@ def orthogonalize(probes) -> None:
 def sweep(args: PtySweepArgs) -> None:
     lib = load()
     check(lib.pty_sweep(C.byref(args), stream_ptr()), "pty_sweep")
+
+
+def sweep_subpixel(args: PtySweepArgs) -> None:
+    lib = load()
+    check(lib.pty_sweep_subpixel(C.byref(args), stream_ptr()), "pty_sweep_subpixel")
 
 
 def sweep_workspace_bytes(dtype: int, window: int, modes: int, n: int, slots: int) -> int:

@@ -57,6 +57,7 @@ class SolverConfig:
     precision: str = "fp32"           # B200 extension: fp32 (complex64) | fp64 (complex128)
     batch_size: int = 1               # B200 extension: >1 = batched semi-parallel update
     propagator: str = "farfield"      # B200 extension: farfield | fresnel (single-FFT Fresnel regime)
+    subpixel_gather: bool = False     # B200 extension: crops at the float position (residual Fourier shift)
 
     def __post_init__(self) -> None:
         if not (0 <= self.alpha_obj <= 1 and 0 <= self.alpha_probe <= 1):
@@ -75,6 +76,10 @@ class SolverConfig:
             raise ParameterError("batch_size must be >= 1")
         if self.propagator not in ("farfield", "fresnel"):
             raise ParameterError(f"propagator must be 'farfield' or 'fresnel', got {self.propagator!r}")
+        if self.subpixel_gather and self.batch_size > 1:
+            raise ParameterError("subpixel_gather is a sequential-sweep extension (batch_size must be 1)")
+        if self.subpixel_gather and self.track_modulus_error:
+            raise ParameterError("track_modulus_error is not available with subpixel_gather")
 
 
 class ReconState:
@@ -531,7 +536,7 @@ def sweep_replicas(states, datasets, config: SolverConfig, orders=None, kernel_e
             raise ParameterError("need one config per state")
         shared = ("alpha_obj", "alpha_probe", "beta", "gamma", "epsilon_rel", "update_probe_modes",
                   "track_modulus_error", "posref", "ortho_interval", "precision", "mode_count",
-                  "batch_size", "propagator")
+                  "batch_size", "propagator", "subpixel_gather")
         for c in configs[1:]:
             if any(getattr(c, k) != getattr(configs[0], k) for k in shared):
                 raise ParameterError("replicas in one launch must share the update rule "
@@ -605,7 +610,10 @@ def sweep_replicas(states, datasets, config: SolverConfig, orders=None, kernel_e
         int(bool(config.track_modulus_error)), sense, _native.ptr(ws), ws.numel())
     if kernel_events is not None:
         kernel_events[0].record()
-    _native.sweep(args)
+    if config.subpixel_gather:
+        _native.sweep_subpixel(args)
+    else:
+        _native.sweep(args)
     if kernel_events is not None:
         kernel_events[1].record()
 

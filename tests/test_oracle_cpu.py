@@ -28,3 +28,31 @@ def test_chaos_control_bounds_trajectory_parity():
     assert gap[9] < 1e-8
     assert gap[19] > 1e-3
     assert abs(a.error_trace[-1] - b.error_trace[-1]) < 1e-2 * a.error_trace[-1]
+
+
+def test_oracle_subpixel_gather_reduces_to_reference_on_integer_grid():
+    """oracle/rpie.py sweep(subpixel_gather): with every residual zero the
+    extension is bit-identical to the reference sweep (no FFT round trip)."""
+    from types import SimpleNamespace
+    import numpy as np
+    from oracle import rpie
+    from scenes import host_scene
+    ds, _, _, _ = host_scene(32, (3, 3), 6.0, 8.0, 1, (1.0,), jitter=0.0, seed=2)
+    pos = np.round(ds.positions)
+    base = dict(alpha_obj=0.9, alpha_probe=0.9, beta=0.5, gamma=0.5, mode_count=1, position_order="shuffled",
+                shuffle_seed=0, init_seed=0, epsilon_rel=1e-12, ortho_interval=0, update_probe_modes=True,
+                posref=None, track_modulus_error=False)
+    a = SimpleNamespace(**base, subpixel_gather=True)
+    b = SimpleNamespace(**base)
+    sa = rpie.initialize(ds.patterns, pos, 32, a)
+    sb = rpie.initialize(ds.patterns, pos, 32, b)
+    for _ in range(2):
+        rpie.sweep(sa, ds.patterns, 32, a)
+        rpie.sweep(sb, ds.patterns, 32, b)
+    assert np.array_equal(sa.obj, sb.obj)
+    assert all(np.array_equal(x, y) for x, y in zip(sa.probes, sb.probes))
+    # and with subpixel residuals the crop really moves
+    c = SimpleNamespace(**base, subpixel_gather=True)
+    sc = rpie.initialize(ds.patterns, pos + 0.3, 32, c)
+    rpie.sweep(sc, ds.patterns, 32, c)
+    assert not np.array_equal(sc.obj, sa.obj)
