@@ -670,6 +670,10 @@ def main():
 
     import torch
     if world > 1:
+        # fixed NCCL algorithm and protocol: the batched mode's collectives then
+        # reduce in the same order on every run (bitwise-reproducible sweeps)
+        os.environ.setdefault("NCCL_ALGO", "Ring")
+        os.environ.setdefault("NCCL_PROTO", "Simple")
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         torch.distributed.init_process_group("nccl")
     res = gpu_arm(args, rank, world)

@@ -177,7 +177,8 @@ PTY_API int pty_check_patterns(const void* patterns, int32_t dtype, int64_t coun
  * Batched (semi-parallel) rPIE, one batch of positions of ONE reconstruction.
  * pty_batch_contrib computes every position of `batch` against the batch-start
  * state and leaves the summed update terms in the caller-owned accumulators:
- *   obj_acc   [3][H][Wc]  real: object numerator (re, im), denominator
+ *   obj_acc   [H][3][Wc]  real: object numerator (re, im), denominator, the three
+ *                         planes interleaved per canvas row (a row band is contiguous)
  *   probe_acc [2M+1][W][W] real: probe numerator (re, im) per mode, denominator
  * (real = float for PTY_DTYPE_C64, double for C128).  Ranks that split a batch
  * all-reduce (sum) both accumulators, then every rank calls pty_batch_apply.
@@ -211,6 +212,9 @@ PTY_API int64_t pty_batch_workspace_bytes(int32_t dtype, int32_t window, int32_t
                                           int32_t n_batch, int32_t H, int32_t Wc);
 PTY_API int pty_batch_contrib(const PtyBatchArgs* args, void* stream);
 PTY_API int pty_batch_apply(const PtyBatchArgs* args, void* stream);
+/* dst[i] += src[i] for n real values of the dtype's real type (an owner rank
+ * adding the halo rows of another rank's object accumulator). */
+PTY_API int pty_accumulate(void* dst, const void* src, int64_t n, int32_t dtype, void* stream);
 PTY_API int pty_batch_finalize(const double* err_part, int32_t n_visits, int32_t window,
                                double* err_out, void* stream);
 

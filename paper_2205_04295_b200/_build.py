@@ -12,12 +12,15 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-LIB = PKG / "libptycho_b200.so"
+LIB = Path(os.environ["PTY_LIB_OUT"]).resolve() if os.environ.get("PTY_LIB_OUT") else PKG / "libptycho_b200.so"
 SOURCES = sorted(CSRC.glob("*.cu"))
 DEPS = sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "ptycho_b200.h"] + SOURCES
-OBJDIR = PKG / "build"
+OBJDIR = PKG / "build" if LIB.parent == PKG and LIB.name == "libptycho_b200.so" else LIB.parent / f"build_{LIB.stem}"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# experiment builds: PTY_NVCC_DEFS="-DX -DY" and PTY_LIB_OUT=<path> build a variant
+# library beside the default one (loaded with PTY_LIB=<path>)
+EXTRA = os.environ.get("PTY_NVCC_DEFS", "").split()
 FLAGS = ["-O3", "-lineinfo", "--std=c++17", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
          "-I", str(ROOT / "include")]
@@ -39,7 +42,7 @@ def needs_build() -> bool:
 
 def _compile(src: Path, verbose: bool):
     obj = OBJDIR / (src.stem + ".o")
-    cmd = [nvcc(), *ARCH, *FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-c", "-o", str(obj), str(src)]
+    cmd = [nvcc(), *ARCH, *FLAGS, *EXTRA, *(["-Xptxas", "-v"] if verbose else []), "-c", "-o", str(obj), str(src)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     return src, obj, res
 

@@ -97,6 +97,7 @@ def _declare(lib):
         "pty_batch_contrib": (C.c_int, [C.POINTER(PtyBatchArgs), vp]),
         "pty_batch_apply": (C.c_int, [C.POINTER(PtyBatchArgs), vp]),
         "pty_batch_finalize": (C.c_int, [vp, i32, i32, vp, vp]),
+        "pty_accumulate": (C.c_int, [vp, vp, i64, i32, vp]),
         "pty_visit_scratch_bytes": (i64, [i32, i32, i32]),
         "pty_magnitude_correct": (C.c_int, [i32, i32, i32, vp, vp, vp, dp, vp, vp, vp, vp, i64, vp]),
         "pty_update_object": (C.c_int, [i32, i32, i32, vp, vp, vp, dp, dp, dp, vp, vp, vp, i64, vp]),
@@ -120,6 +121,7 @@ EXPORTS = ("pty_abi_version", "pty_launch_count", "pty_barrier_bench", "pty_time
            "pty_fft2", "pty_register_batch", "pty_register_scratch_bytes", "pty_adam_apply",
            "pty_init_probes", "pty_orthogonalize", "pty_check_patterns",
            "pty_batch_workspace_bytes", "pty_batch_contrib", "pty_batch_apply", "pty_batch_finalize",
+           "pty_accumulate",
            "pty_visit_scratch_bytes", "pty_magnitude_correct", "pty_update_object", "pty_update_probe",
            "pty_cross_power_spectrum", "pty_coarse_argmax", "pty_upsampled_idft_scratch_bytes",
            "pty_upsampled_idft", "pty_argmax_abs", "pty_adam_step", "pty_apply_correction")
@@ -297,6 +299,14 @@ def batch_contrib(args: PtyBatchArgs) -> None:
 
 def batch_apply(args: PtyBatchArgs) -> None:
     check(load().pty_batch_apply(C.byref(args), stream_ptr()), "pty_batch_apply")
+
+
+def accumulate(dst, src) -> None:
+    """dst += src (contiguous real CUDA tensors of one dtype, same size)."""
+    if dst.numel() != src.numel() or not dst.is_contiguous() or not src.is_contiguous():
+        raise NativeError("accumulate needs two contiguous tensors of one size")
+    check(load().pty_accumulate(ptr(dst), ptr(src), dst.numel(), dtype_code(dst), stream_ptr()),
+          "pty_accumulate")
 
 
 def batch_finalize(err_part, n_visits: int, window: int, err_out) -> None:

@@ -44,7 +44,7 @@ struct BatchDev {
     double alpha_o, alpha_p, beta, gamma, eps_rel;
     int update_probe, track_mod, sense;
     void* stage;                       // [N][2][W][W] complex or null
-    void* obj_acc;                     // [3][H][Wc] real: num.re, num.im, den
+    void* obj_acc;                     // [H][3][Wc] real: num.re, num.im, den (planes interleaved per row)
     void* probe_acc;                   // [2M+1][W][W] real: pnum (re, im) per mode, pden
     double* err_part;                  // [N][W][3] by visit rank (visit0 + k)
     int* status;
@@ -401,10 +401,10 @@ __global__ void __launch_bounds__(256) bk_obj_gather(const __grid_constant__ Bat
     for (int q = 0; q < PX; ++q) {
         const int p = threadIdx.x + q * 256, R = R0 + p / kObjTile, Cc = C0 + p % kObjTile;
         if (R < P.H && Cc < P.Wc) {
-            const size_t o = (size_t)R * P.Wc + Cc;
+            const size_t o = (size_t)R * 3 * P.Wc + Cc;
             acc[o] += num[q].re;                      // chunks add in a fixed order
-            acc[HW + o] += num[q].im;
-            acc[2 * HW + o] += den[q];
+            acc[P.Wc + o] += num[q].im;
+            acc[2 * P.Wc + o] += den[q];
         }
     }
 }
@@ -415,11 +415,11 @@ __global__ void __launch_bounds__(256) bk_obj_tile_max(const __grid_constant__ B
     __shared__ T red[32];
     const int tiles_x = (P.Wc + kObjTile - 1) / kObjTile;
     const int ty = blockIdx.x / tiles_x, tx = blockIdx.x % tiles_x;
-    const T* den = reinterpret_cast<const T*>(P.obj_acc) + 2 * (size_t)P.H * P.Wc;
+    const T* den = reinterpret_cast<const T*>(P.obj_acc) + 2 * (size_t)P.Wc;
     T m = T(0);
     for (int p = threadIdx.x; p < kObjTile * kObjTile; p += blockDim.x) {
         const int R = ty * kObjTile + p / kObjTile, Cc = tx * kObjTile + p % kObjTile;
-        if (R < P.H && Cc < P.Wc) m = fmax(m, den[(size_t)R * P.Wc + Cc]);
+        if (R < P.H && Cc < P.Wc) m = fmax(m, den[(size_t)R * 3 * P.Wc + Cc]);
     }
     m = block_max(m, red);
     if (threadIdx.x == 0) reinterpret_cast<T*>(P.tile_max)[blockIdx.x] = m;
@@ -445,11 +445,12 @@ __global__ void __launch_bounds__(256) bk_obj_apply(const __grid_constant__ Batc
     C* upd = reinterpret_cast<C*>(P.upd);
     const T alpha_o = T(P.alpha_o), eps_rel = T(P.eps_rel);
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < HW; i += (size_t)gridDim.x * blockDim.x) {
-        const T den = acc[2 * HW + i];
+        const size_t a = (i / P.Wc) * 3 * P.Wc + i % P.Wc;          // [R][plane][C]
+        const T den = acc[a + 2 * P.Wc];
         const C o = obj[i];
         C u = o;
         if (den > T(0)) {
-            u = o + divr(scale(C{acc[i], acc[HW + i]}, alpha_o), den + eps_rel * dmax);
+            u = o + divr(scale(C{acc[a], acc[a + P.Wc]}, alpha_o), den + eps_rel * dmax);
             obj[i] = o + (u - o);
         }
         if (upd) upd[i] = u;

@@ -50,9 +50,12 @@ struct SweepDev {
     int slot_local;               // every phase's tasks of slot s live on CTAs [s*cps, (s+1)*cps): per-slot barriers
     int cps;                      // CTAs per slot (slot_local)
     unsigned int* slot_bar;       // [nslots][32] per-slot barrier counters (slot_local)
+    int pair;                     // > 0: slots s and s + spp share the same SMs (virtual CTA index below)
+    unsigned int* sm_pair;        // [8 + 256]: SM-id bitmap, CTAs per SM (zeroed per launch)
     // workspace
     unsigned int* barrier;
     int* anchors;                 // [nslots][N][2]
+    int4* steptab;                // [nslots][N]: (j, ar, ac, 0) of visit step t (order[t] and its anchor)
     void* scratch;                // [nslots][M][W][W] complex, transposed after the row pass
     void* totT;                   // [nslots][W][W] real
     void* omax_part;              // [nslots][W/4] real
@@ -163,6 +166,8 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // per-step snapshot of every slot: dead flag, position index, anchor
     __shared__ int s_dead[kMaxSlots], s_j[kMaxSlots], s_ar[kMaxSlots], s_ac[kMaxSlots];
+    __shared__ unsigned long long s_mbar[NGRP];               // one bulk-copy barrier per line group
+    unsigned mphase = 0u;                                      // its parity (identical on the group's lanes)
     C* tw = reinterpret_cast<C*>(smem_raw);
     T* red = reinterpret_cast<T*>(smem_raw + (size_t)W * sizeof(C));
     unsigned char* region = smem_raw + sweep_smem_fixed<T, W>();
@@ -173,6 +178,7 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
     const int s0 = CL ? (int)cluster_index() : 0;
     const int S = CL ? 1 : P.nslots;                       // slots walked by this CTA set
     const int cta = CL ? (int)cluster_rank() : (int)blockIdx.x;
+    int vcta = cta;                                        // task-enumeration index (SM-paired in slot-local mode)
     const int ncta = CL ? (int)cluster_size() : (int)gridDim.x;
     const size_t WW = (size_t)W * W;
     const int nq = W / 4;
@@ -228,6 +234,8 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
         }
     };
     load_twiddles<T, W>(tw, reinterpret_cast<const C*>(P.twiddles));
+    if (tid < NGRP) mbar_init(&s_mbar[tid], 1u);
+    __syncthreads();
 
     // ---- phase 0: anchors (engine.py:69-70, 192-195) + bounds, initial probe peak
     for (int li = cta * NT + tid; li < S * N; li += ncta * NT) {
@@ -240,6 +248,10 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
         P.anchors[2 * idx] = ar;
         P.anchors[2 * idx + 1] = ac;
         if (ar < 0 || ac < 0 || ar + W > sl.H || ac + W > sl.Wc) atomicOr(sl.status, PTY_ERR_BOUNDS);
+        // step table: the visit at step t = j is order[t]; its anchor needs no second lookup
+        const int t = j, jt = sl.order[t];
+        const double xt = sl.positions[2 * jt], yt = sl.positions[2 * jt + 1];
+        P.steptab[idx] = make_int4(jt, (int)rint(yt) - sl.r0, (int)rint(xt) - sl.c0, 0);
     }
     for (int item = cta; item < S * nq; item += ncta) {
         const int s = s0 + item / nq, rq = item % nq;
@@ -256,10 +268,33 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
         pk = block_max(pk, red);
         if (tid == 0) peak_part[(size_t)s * nq + rq] = pk;
     }
+    // SM pairing: register this CTA's SM (bitmap) and its rank among the CTAs on it
+    __shared__ int s_vcta;
+    unsigned my_sm = 0, my_rank = 0;
+    if (!CL && P.pair > 0 && tid == 0) {
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(my_sm));
+        my_sm &= 255u;
+        atomicOr(&P.sm_pair[my_sm >> 5], 1u << (my_sm & 31));
+        my_rank = atomicAdd(&P.sm_pair[8 + my_sm], 1u);
+    }
     phase_sync();
     if constexpr (!CL) {
         if (P.slot_local) {
-            const int my_slot = (int)blockIdx.x / P.cps;
+            // slots s and s + spp get the same SM set: virtual CTA = rank on the
+            // SM * pair + dense index of the SM, so both CTAs of an SM serve the
+            // same CTA position of two slots and every CTA of a slot sees the
+            // same neighbour (uniform contention, balanced phases)
+            if (P.pair > 0) {
+                if (tid == 0) {
+                    unsigned below = 0;
+                    for (unsigned w = 0; w < (my_sm >> 5); ++w) below += __popc(P.sm_pair[w]);
+                    below += __popc(P.sm_pair[my_sm >> 5] & ((1u << (my_sm & 31)) - 1u));
+                    s_vcta = (my_rank < 2u && (int)below < P.pair) ? (int)my_rank * P.pair + (int)below : 0x3fffffff;
+                }
+                __syncthreads();
+                vcta = s_vcta;
+            }
+            const int my_slot = vcta / P.cps;
             if (my_slot >= S) return;                          // idle CTA: no task in any phase
             local = true;
             my_bar = P.slot_bar + 32 * my_slot;
@@ -276,19 +311,27 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
         stamp(step, 0);
         if (tid < S) {   // status only changes in P4 / phase 0, both behind a barrier
             const int s = s0 + tid;
+#ifndef PTY_NO_STEPTAB
+            const int4 v = P.steptab[(size_t)s * N + step];     // (j, ar, ac): one load, no dependent lookup
+            s_dead[s] = *(volatile const int*)P.slot[s].status;
+            s_j[s] = v.x;
+            s_ar[s] = v.y;
+            s_ac[s] = v.z;
+#else
             const SlotDev& sl = P.slot[s];
             const int j = sl.order[step];
             s_dead[s] = *(volatile const int*)sl.status;
             s_j[s] = j;
             s_ar[s] = P.anchors[2 * (s * N + j)];
             s_ac[s] = P.anchors[2 * (s * N + j) + 1];
+#endif
         }
         __syncthreads();
         // ---------------------------------------------------------- P1 rows
         if (P.p4_staged && P.p1_staged) {
             C* lines_m = reinterpret_cast<C*>(region) + (size_t)team * M * 4 * LS4;
             T* red4_s = reinterpret_cast<T*>(reinterpret_cast<C*>(region) + (size_t)NTEAM * M * 4 * LS4) + team * 4;
-            for (int task = cta * NTEAM + team; task < S * nq; task += ncta * NTEAM) {
+            for (int task = vcta * NTEAM + team; task < S * nq; task += ncta * NTEAM) {
                 const int s = s0 + task / nq, rq = task % nq;
                 if (s_dead[s]) continue;
                 const SlotDev& sl = P.slot[s];
@@ -301,7 +344,7 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
                 T om;
 #define PTY_P1S(MM) om = task_row_fwd_staged<T, W, MM>(tw, lines_m, red4_s, team, tl, gi, b, gmask, \
                     reinterpret_cast<const C*>(sl.obj), sl.Wc, s_ar[s], s_ac[s], reinterpret_cast<const C*>(sl.probes), rq, \
-                    scratch + (size_t)s * M * WW, stg)
+                    scratch + (size_t)s * M * WW, stg, &s_mbar[grp], &mphase)
                 switch (M) {
                     case 1: PTY_P1S(1); break;
                     case 2: PTY_P1S(2); break;
@@ -312,7 +355,7 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
                 if (tl == 0) omax_part[(size_t)s * nq + rq] = om;
             }
         } else
-        for (int task = cta * NTEAM + team; task < S * M * nq; task += ncta * NTEAM) {
+        for (int task = vcta * NTEAM + team; task < S * M * nq; task += ncta * NTEAM) {
             const int s = s0 + task / (M * nq), m = (task / nq) % M, rq = task % nq;
             if (s_dead[s]) continue;
             const SlotDev& sl = P.slot[s];
@@ -334,11 +377,12 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
         phase_sync();
         stamp(step, 2);
         // ------------------------------------------------- P2 cols (forward)
-        for (int task = cta * NGRP + grp; task < S * W; task += ncta * NGRP) {
+        for (int task = vcta * NGRP + grp; task < S * W; task += ncta * NGRP) {
             const int s = s0 + task / W, kc = task % W;
             if (s_dead[s]) continue;
             const T tm = P.resident
-                ? task_col_fwd<T, W, true>(tw, xch, b, gmask, scratch + (size_t)s * M * WW, M, kc, totT + (size_t)s * WW, res)
+                ? task_col_fwd<T, W, true>(tw, xch, b, gmask, scratch + (size_t)s * M * WW, M, kc, totT + (size_t)s * WW, res,
+                                           &s_mbar[grp], &mphase)
                 : task_col_fwd<T, W, false>(tw, xch, b, gmask, scratch + (size_t)s * M * WW, M, kc, totT + (size_t)s * WW);
             if (b == 0) tmax_part[(size_t)s * W + kc] = tm;
         }
@@ -346,7 +390,7 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
         phase_sync();
         stamp(step, 4);
         // ---------------------------------------- P3 modulus + cols (inverse)
-        for (int task = cta * NGRP + grp; task < S * W; task += ncta * NGRP) {
+        for (int task = vcta * NGRP + grp; task < S * W; task += ncta * NGRP) {
             const int s = s0 + task / W, kc = task % W;
             if (s_dead[s]) continue;
             const SlotDev& sl = P.slot[s];
@@ -365,7 +409,7 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
         phase_sync();
         stamp(step, 6);
         // --------------------------------------- P4 rows (inverse) + update
-        for (int task = cta * NTEAM + team; task < S * nq; task += ncta * NTEAM) {
+        for (int task = vcta * NTEAM + team; task < S * nq; task += ncta * NTEAM) {
             const int s = s0 + task / nq, rq = task % nq;
             if (s_dead[s]) continue;
             const SlotDev& sl = P.slot[s];

@@ -13,6 +13,7 @@ namespace pty {
 struct SweepLayout {
     unsigned int* barrier;
     int* anchors;
+    int4* steptab;
     void* scratch;
     void* totT;
     void* omax;
@@ -22,6 +23,7 @@ struct SweepLayout {
     double* visit_sum;
     void* ppg;
     unsigned int* slot_bar;
+    unsigned int* sm_pair;
     size_t bytes;
 };
 
@@ -31,6 +33,7 @@ inline SweepLayout carve_sweep(void* ws, int W, int M, int N, int S) {
     SweepLayout L{};
     L.barrier = c.take<unsigned int>(sizeof(unsigned int));
     L.anchors = c.take<int>((size_t)S * N * 2 * sizeof(int));
+    L.steptab = c.take<int4>((size_t)S * N * sizeof(int4));
     L.scratch = c.take<void>((size_t)S * M * W * W * sizeof(cplx<T>));
     L.totT = c.take<void>((size_t)S * W * W * sizeof(T));
     L.omax = c.take<void>((size_t)S * (W / 4) * sizeof(T));
@@ -40,6 +43,7 @@ inline SweepLayout carve_sweep(void* ws, int W, int M, int N, int S) {
     L.visit_sum = c.take<double>((size_t)S * N * 3 * sizeof(double));
     L.ppg = c.take<void>((size_t)S * W * W * sizeof(T));
     L.slot_bar = c.take<unsigned int>((size_t)S * 32 * sizeof(unsigned int));
+    L.sm_pair = c.take<unsigned int>((8 + 256) * sizeof(unsigned int));
     L.bytes = c.off;
     return L;
 }
@@ -77,7 +81,7 @@ int run_sweep_lines(const PtySweepArgs* a, cudaStream_t st) {
     P.alpha_o = a->alpha_obj; P.alpha_p = a->alpha_probe; P.beta = a->beta; P.gamma = a->gamma;
     P.eps_rel = a->epsilon_rel;
     P.update_probe = a->update_probe; P.track_mod = a->track_modulus; P.sense = a->sense;
-    P.barrier = L.barrier; P.anchors = L.anchors; P.scratch = L.scratch; P.totT = L.totT;
+    P.barrier = L.barrier; P.anchors = L.anchors; P.steptab = L.steptab; P.scratch = L.scratch; P.totT = L.totT;
     P.omax_part = L.omax; P.peak_part = L.peak; P.tmax_part = L.tmax;
     P.err_part = L.err_part; P.twiddles = tw; P.ppg = L.ppg;
     ErrOut outs{};
@@ -165,6 +169,10 @@ int run_sweep_lines(const PtySweepArgs* a, cudaStream_t st) {
                         cps_rows == cps_cols && cps_rows >= 1 && (long)S * cps_rows <= grid &&
                         (W / 4) % NTEAM4 == 0 && W % NGRP == 0) ? 1 : 0;
         P.slot_bar = L.slot_bar;
+        // two slots per SM set when the slots outnumber one CTA per SM
+        const int spp = (grid / 2) / std::max(1, cps_rows);
+        P.pair = (P.slot_local && per_sm == 2 && S > spp && S <= 2 * spp && env_int("PTY_SLOT_PAIR", 0)) ? spp * cps_rows : 0;
+        P.sm_pair = L.sm_pair;
     }
 
     // debug timeline (PTY_TIMELINE=<steps>): per-CTA phase completion stamps
@@ -177,6 +185,7 @@ int run_sweep_lines(const PtySweepArgs* a, cudaStream_t st) {
     }
     if (cudaMemsetAsync(L.barrier, 0, sizeof(unsigned int), st) != cudaSuccess) return PTY_ERR_CUDA;
     if (cudaMemsetAsync(L.slot_bar, 0, (size_t)S * 32 * sizeof(unsigned int), st) != cudaSuccess) return PTY_ERR_CUDA;
+    if (cudaMemsetAsync(L.sm_pair, 0, (8 + 256) * sizeof(unsigned int), st) != cudaSuccess) return PTY_ERR_CUDA;
     if (cudaMemsetAsync(L.err_part, 0, (size_t)S * N * W * 3 * sizeof(double), st) != cudaSuccess)
         return PTY_ERR_CUDA;
     cudaError_t e;

@@ -127,27 +127,43 @@ __device__ __forceinline__ T task_row_fwd(const cplx<T>* tw, cplx<T>* xch, cplx<
 }
 
 // Row pass, staged variant: team task (row quad rq, ALL modes) of one
-// position.  The object rows are loaded once and kept in registers; for each
-// mode the probe row is loaded, the exit wave staged in the team's lines
-// (lines[(m*4 + gi)*LS4 + pad(n)]); then every line is transformed in place
-// and written transposed ([m][kc][r]) straight from the lines.  Same
-// arithmetic as task_row_fwd.  Returns the team's max|o|^2.
+// position.  Every mode's probe row is brought into the group's mode lines by
+// bulk copies (one elected lane, the group's mbarrier) while the object row is
+// loaded into registers, so all of the task's inputs are in flight at once;
+// each line is then overwritten in place by its exit wave
+// (lines[(m*4 + gi)*LS4 + pad(n)]), transformed, and written transposed
+// ([m][kc][r]) straight from the lines.  Same arithmetic as task_row_fwd.
+// Returns the team's max|o|^2.
 template <typename T, int W, int MODES>
 __device__ __forceinline__ T task_row_fwd_staged(const cplx<T>* tw, cplx<T>* lines, T* red4, int team, int tl, int gi,
                                                  int b, unsigned gmask, const cplx<T>* obj, int Wc, int ar, int ac,
-                                                 const cplx<T>* probes, int rq, cplx<T>* dst_pos, cplx<T>* stg_o) {
+                                                 const cplx<T>* probes, int rq, cplx<T>* dst_pos, cplx<T>* stg_o,
+                                                 unsigned long long* mbar, unsigned* mphase) {
     using C = cplx<T>;
     constexpr int A = Shape<W>::A, B = Shape<W>::B, TEAM = 4 * B, LS4 = team_line_stride<W>();
     const size_t WW = (size_t)W * W;
     const int r = 4 * rq + gi;
     const C* orow = obj + (size_t)(ar + r) * Wc + ac;
     const C* prow = probes + (size_t)r * W;
+#ifdef PTY_TMA_LINES
+    if (b == 0) {
+        fence_proxy_async();
+        mbar_expect_tx(mbar, (unsigned)(MODES * W * sizeof(C)));
+#pragma unroll
+        for (int m = 0; m < MODES; ++m)
+            bulk_g2s(lines + (m * 4 + gi) * LS4, prow + m * WW, (unsigned)(W * sizeof(C)), mbar);
+    }
+    C ov[A], pv[A];
+#pragma unroll
+    for (int a = 0; a < A; ++a) ov[a] = orow[B * a + b];
+#else
     C ov[A], pv[A];
 #pragma unroll
     for (int a = 0; a < A; ++a) {
         ov[a] = orow[B * a + b];
         pv[a] = prow[B * a + b];
     }
+#endif
     T om = T(0);
 #pragma unroll
     for (int a = 0; a < A; ++a) om = fmax(om, norm2(ov[a]));
@@ -156,6 +172,22 @@ __device__ __forceinline__ T task_row_fwd_staged(const cplx<T>* tw, cplx<T>* lin
 #pragma unroll
         for (int a = 0; a < A; ++a) stg[B * a + b] = ov[a];
     }
+#ifdef PTY_TMA_LINES
+    mbar_wait(mbar, *mphase);
+    *mphase ^= 1u;
+#pragma unroll
+    for (int m = 0; m < MODES; ++m) {
+        C* line = lines + (m * 4 + gi) * LS4;
+#pragma unroll
+        for (int a = 0; a < A; ++a) pv[a] = line[B * a + b];          // P_m row, contiguous
+        __syncwarp(gmask);
+#pragma unroll
+        for (int a = 0; a < A; ++a) {
+            const int n = B * a + b;
+            line[pad<W>(n)] = scale(pv[a] * ov[a], checker<T>(r, n));
+        }
+    }
+#else
     team_sync<TEAM>(team);                                    // lines free
 #pragma unroll
     for (int m = 0; m < MODES; ++m) {
@@ -170,6 +202,7 @@ __device__ __forceinline__ T task_row_fwd_staged(const cplx<T>* tw, cplx<T>* lin
             line[pad<W>(n)] = scale(pv[a] * ov[a], checker<T>(r, n));
         }
     }
+#endif
     __syncwarp(gmask);
 #pragma unroll 1
     for (int m = 0; m < MODES; ++m) line_fft<T, W, false>(lines + (m * 4 + gi) * LS4, tw, b, gmask);
@@ -191,9 +224,13 @@ __device__ __forceinline__ T task_row_fwd_staged(const cplx<T>* tw, cplx<T>* lin
 // every mode written back in place (Psi), total = sum_m |Psi_m|^2 (engine.py:
 // 114-116) stored transposed; returns the column's max(total).  STORE = false
 // keeps Psi off HBM (the batched column pass 2 recomputes it, REFWD below).
+// RES: the M column lines are brought into the group's resident shared-memory
+// lines by bulk copies (one elected lane, one mbarrier per group: every mode's
+// line in flight at once, no registers), then transformed in place.
 template <typename T, int W, bool RES = false, bool STORE = true>
 __device__ __forceinline__ T task_col_fwd(const cplx<T>* tw, cplx<T>* xch, int b, unsigned gmask, cplx<T>* pos, int M,
-                                          int kc, T* totT_pos, cplx<T>* res = nullptr) {
+                                          int kc, T* totT_pos, cplx<T>* res = nullptr,
+                                          unsigned long long* mbar = nullptr, unsigned* mphase = nullptr) {
     using C = cplx<T>;
     constexpr int A = Shape<W>::A, B = Shape<W>::B;
     const size_t WW = (size_t)W * W;
@@ -201,12 +238,28 @@ __device__ __forceinline__ T task_col_fwd(const cplx<T>* tw, cplx<T>* xch, int b
     T tot[A];
 #pragma unroll
     for (int q = 0; q < A; ++q) tot[q] = T(0);
+#ifdef PTY_TMA_LINES
+    if constexpr (RES) {
+        if (b == 0) {
+            fence_proxy_async();
+            mbar_expect_tx(mbar, (unsigned)(M * W * sizeof(C)));
+            for (int m = 0; m < M; ++m)
+                bulk_g2s(res + m * xch_size<W>(), pos + m * WW + (size_t)kc * W, (unsigned)(W * sizeof(C)), mbar);
+        }
+        mbar_wait(mbar, *mphase);
+        *mphase ^= 1u;
+    }
+#endif
     for (int m = 0; m < M;++m) {
         C* line = pos + m * WW + (size_t)kc * W;
         if constexpr (RES) {   // Psi_m stays in this group's shared-memory line for P3
             C* rl = res + m * xch_size<W>();
             group_fft<T, W, false>(
+#ifdef PTY_TMA_LINES
+                rl, tw, b, gmask, [&](int n, int) { return rl[n]; },
+#else
                 rl, tw, b, gmask, [&](int n, int) { return line[n]; },
+#endif
                 [&](int u, int slot, C v) {
                     rl[pad<W>(u)] = v;
                     tot[slot] += norm2(v) * invW2;
@@ -261,7 +314,7 @@ __device__ __forceinline__ void task_col_mod(const cplx<T>* tw, cplx<T>* xch, in
     }
     tmax = group_max<B>(tmax);
     const T eps = eps_rel * fmax(tmax, real_limits<T>::tiny());
-    T sc[A], after[A];
+    T sc[A];
     double en = 0.0, ed = 0.0;
 #pragma unroll
     for (int a = 0; a < A; ++a) {
@@ -272,34 +325,44 @@ __device__ __forceinline__ void task_col_mod(const cplx<T>* tw, cplx<T>* xch, in
         const T d = sqrt_fast(tv) - sI;
         en += (double)(d * d);
         ed += (double)Iv;
-        after[a] = T(0);
         if (stg) {
             stg[(size_t)u * W + kc] = C{tv, T(0)};
             stg[WW + (size_t)u * W + kc] = C{Iv, T(0)};
         }
     }
-    for (int m = 0; m < M; ++m) {
-        C* line = pos + m * WW + (size_t)kc * W;
-        C* rl = RES ? res + m * xch_size<W>() : xch;      // resident Psi_m from P2
-        if constexpr (REFWD) {
-            group_fft<T, W, false>(
-                xch, tw, b, gmask, [&](int n, int) { return line[n]; }, [&](int u, int, C v) { xch[pad<W>(u)] = v; });
-            __syncwarp(gmask);
+    // I and total are dead here (reloaded below for the diagnostic): only the
+    // A scales stay live across the mode loop
+    auto inverse_cols = [&](auto&& on_input) {
+        for (int m = 0; m < M; ++m) {
+            C* line = pos + m * WW + (size_t)kc * W;
+            C* rl = RES ? res + m * xch_size<W>() : xch;      // resident Psi_m from P2
+            if constexpr (REFWD) {
+                group_fft<T, W, false>(
+                    xch, tw, b, gmask, [&](int n, int) { return line[n]; },
+                    [&](int u, int, C v) { xch[pad<W>(u)] = v; });
+                __syncwarp(gmask);
+            }
+            group_fft<T, W, true>(
+                rl, tw, b, gmask,
+                [&](int n, int a) {
+                    const C v = scale((RES || REFWD) ? rl[pad<W>(n)] : line[n], sc[a]);
+                    on_input(a, v);
+                    return v;
+                },
+                [&](int r, int, C v) { line[r] = v; });
         }
-        group_fft<T, W, true>(
-            rl, tw, b, gmask,
-            [&](int n, int a) {
-                const C v = scale((RES || REFWD) ? rl[pad<W>(n)] : line[n], sc[a]);
-                after[a] += norm2(v) * invW2;
-                return v;
-            },
-            [&](int r, int, C v) { line[r] = v; });
-    }
+    };
     T worst = T(0);
-    if (track) {
+    if (!track) {
+        inverse_cols([](int, C) {});
+    } else {                                           // modulus diagnostic (engine.py:204-214)
+        T after[A];
+#pragma unroll
+        for (int a = 0; a < A; ++a) after[a] = T(0);
+        inverse_cols([&](int a, C v) { after[a] += norm2(v) * invW2; });
 #pragma unroll
         for (int a = 0; a < A; ++a) {
-            const T Iv = Ia[a], tv = ta[a];
+            const T Iv = It[B * a + b], tv = tt[B * a + b];
             if (tv > T(1e-3) * tmax) worst = fmax(worst, fabs(after[a] - Iv) / fmax(Iv, real_limits<T>::tiny()));
         }
     }
@@ -453,6 +516,23 @@ __device__ __forceinline__ T task_row_inv_update(const cplx<T>* tw, cplx<T>* lin
 // gathered first and its accumulators in registers.  Same expressions and
 // mode order as task_row_inv_update (engine.py:119-150, 218-224,
 // fields.py:101-107).  Returns the team max of the next visit's sum_m |P_m|^2.
+// Every mode's 4 scratch rows of row quad rq straight into the team's lines
+// (LDGSTS: all 4 * W * MODES elements in flight at once, no register staging);
+// the caller waits with cp_async_wait_all() + a team sync.
+template <typename T, int W, int MODES>
+__device__ __forceinline__ void stage_rows_async(cplx<T>* lines, const cplx<T>* pos, int rq, int tl) {
+    constexpr int B = Shape<W>::B, TEAM = 4 * B, LS4 = team_line_stride<W>(), NE = 4 * W / TEAM;
+    const size_t WW = (size_t)W * W;
+#pragma unroll
+    for (int m = 0; m < MODES; ++m)
+#pragma unroll
+        for (int i = 0; i < NE; ++i) {
+            const int e = tl + i * TEAM;
+            cp_async<(int)sizeof(cplx<T>)>(&lines[(m * 4 + (e & 3)) * LS4 + pad<W>(e >> 2)],
+                                           &pos[m * WW + (size_t)(e >> 2) * W + 4 * rq + (e & 3)]);
+        }
+}
+
 template <typename T, int W, int MODES>
 __device__ __forceinline__ T task_row_inv_update_staged(const cplx<T>* tw, cplx<T>* lines, T* red4, int team,
                                                         int tl, int gi, int b, unsigned gmask, const cplx<T>* pos,
@@ -461,11 +541,16 @@ __device__ __forceinline__ T task_row_inv_update_staged(const cplx<T>* tw, cplx<
                                                         cplx<T>* stg) {
     using C = cplx<T>;
     constexpr int B = Shape<W>::B, TEAM = 4 * B, LS4 = team_line_stride<W>(), NE = 4 * W / TEAM;
+#ifdef PTY_P4_CH
+    constexpr int CH = MODES <= 3 ? PTY_P4_CH : (MODES <= 6 ? 2 : 1);
+#else
     constexpr int CH = MODES <= 3 ? 4 : (MODES <= 6 ? 2 : 1);
+#endif
     const size_t WW = (size_t)W * W;
     const T invW2 = T(1) / (T(W) * T(W));
     const T alpha_o = T(U.alpha_o), alpha_p = T(U.alpha_p), beta = T(U.beta), gamma = T(U.gamma),
             eps_rel = T(U.eps_rel);
+#ifndef PTY_P4_LDGSTS
     // the scratch rows of mode m+1 are in flight before mode m is stored to
     // shared memory (two modes of loads outstanding per thread)
     C cur[NE], nxt[NE];
@@ -495,6 +580,11 @@ __device__ __forceinline__ T task_row_inv_update_staged(const cplx<T>* tw, cplx<
         }
     }
     team_sync<TEAM>(team);
+#else
+    stage_rows_async<T, W, MODES>(lines, pos, rq, tl);
+    cp_async_wait_all();
+    team_sync<TEAM>(team);
+#endif
 #pragma unroll 1
     for (int m = 0; m < MODES; ++m) line_fft<T, W, true>(lines + (m * 4 + gi) * LS4, tw, b, gmask);
     team_sync<TEAM>(team);

@@ -299,11 +299,31 @@ __global__ void vis_apply_correction_kernel(double* pos, int j, double dx, doubl
     *inside = (cx == x && cy == y) ? 1 : 0;
 }
 
+// dst[i] += src[i] over n real values (batched mode: an owner adds the halo
+// rows of the object accumulator received from another rank, in rank order)
+template <typename T>
+__global__ void __launch_bounds__(kVisThreads) vis_accumulate_kernel(T* dst, const T* src, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        dst[i] += src[i];
+}
+
 }  // namespace pty
 
 using namespace pty;
 
 extern "C" {
+
+int pty_accumulate(void* dst, const void* src, int64_t n, int32_t dtype, void* stream) {
+    if (!dst || !src || n < 0) return PTY_ERR_ARGUMENT;
+    if (n == 0) return PTY_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    return with_dtype(dtype, [&](auto t) {
+        using T = decltype(t);
+        vis_accumulate_kernel<T><<<vis_blocks(n), kVisThreads, 0, st>>>(static_cast<T*>(dst), static_cast<const T*>(src), n);
+        count();
+        return last_status();
+    });
+}
 
 int64_t pty_visit_scratch_bytes(int32_t dtype, int32_t W, int32_t M) {
     if (!valid_window(W) || M < 1 || M > 8) return -1;

@@ -363,18 +363,62 @@ def sweep(state: ReconState, dataset, config: SolverConfig, group=None) -> Recon
     return state
 
 
-def batch_slice(n_batch: int, rank: int, world: int) -> tuple[int, int]:
-    """Contiguous share [lo, hi) of a batch of n_batch positions for one rank."""
-    base, extra = divmod(n_batch, world)
-    lo = rank * base + min(rank, extra)
-    return lo, lo + base + (1 if rank < extra else 0)
+from .partition import batch_slice, halo_transfers, ownership, rank_shares, row_bands  # noqa: E402
+
+
+def _exchange_object_terms(obj_acc, owns, xfers, rank, world, group) -> None:
+    """Complete a batch's object accumulator on every rank (partition.py):
+    halo rows go to their owner (point-to-point), the owner adds them in rank
+    order, then every rank's owned rows are all-gathered.  The rows no rank
+    touched are zero everywhere already."""
+    import torch.distributed as dist
+    t = _native.torch()
+    host = dist.get_backend(group) == "gloo"          # gloo point-to-point needs host tensors
+    flat = obj_acc.view(obj_acc.shape[0], -1)          # [rows][3 * Wc]: a row band is contiguous
+    dev = flat.device
+    ops, recvs = [], []
+    for src, dst, a, b in xfers:
+        if src == rank:
+            buf = flat[a:b].contiguous()
+            ops.append(dist.P2POp(dist.isend, buf.cpu() if host else buf, dst, group))
+        elif dst == rank:
+            buf = t.empty((b - a, flat.shape[1]), dtype=flat.dtype, device="cpu" if host else dev)
+            ops.append(dist.P2POp(dist.irecv, buf, src, group))
+            recvs.append((a, b, buf))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    for a, b, buf in recvs:                            # xfers order = source rank order
+        _native.accumulate(flat[a:b], buf.to(dev).contiguous())
+    rows = [hi - lo for lo, hi in owns]
+    R = max(rows)
+    if R == 0:
+        return
+    lo, hi = owns[rank]
+    send = t.zeros((R, flat.shape[1]), dtype=flat.dtype, device=dev)
+    if hi > lo:
+        send[:hi - lo].copy_(flat[lo:hi])
+    if host:
+        send = send.cpu()
+    parts = [t.empty_like(send) for _ in range(world)]
+    dist.all_gather(parts, send, group=group)
+    for q, (qlo, qhi) in enumerate(owns):
+        if q != rank and qhi > qlo:
+            flat[qlo:qhi].copy_(parts[q][:qhi - qlo].to(dev))
 
 
 def sweep_batched(state: ReconState, dataset, config: SolverConfig, group=None) -> ReconState:
     """Batched rPIE sweep (extension; b = config.batch_size).  Every batch is a
     contiguous slice of the visit order; its positions see the batch-start
-    state; numerators/denominators are summed (per rank, then NCCL all-reduce
-    across ``group``) and applied once (pty_batch_contrib / pty_batch_apply)."""
+    state; numerators/denominators are summed and applied once
+    (pty_batch_contrib / pty_batch_apply).
+
+    With a process group (``group``, NCCL on GPUs) every batch is split
+    spatially across the ranks (partition.py): each rank accumulates the
+    update terms of its row band, halo rows are sent to their owners, the
+    owned rows are all-gathered and every rank applies the identical update;
+    the probe terms are all-reduced.  Error terms are reduced to three
+    scalars per rank and summed once per sweep."""
     t = _native.torch()
     t0 = time.perf_counter()
     st, ds = state, dataset
@@ -403,82 +447,96 @@ def sweep_batched(state: ReconState, dataset, config: SolverConfig, group=None) 
     err = st.buffer("err", (3,), t.float64)
     err_part = st.buffer("err_part", (n, w, 3), t.float64)
     err_part.zero_()
-    obj_acc = st.buffer("obj_acc", (3, h, wc), rdt)
+    obj_acc = st.buffer("obj_acc", (h, 3, wc), rdt)
     probe_acc = st.buffer("probe_acc", (2 * m + 1, w, w), rdt)
     stage = st.buffer("stage", (n, 2, w, w), cdt) if engaged else None
-    order_h = st.buffer("order", (n,), t.int32, pinned=True)
-    order_h.numpy()[:] = order
-    order_d = st.buffer("order", (n,), t.int32)
-    order_d.copy_(order_h, non_blocking=True)
     ws = _native.workspace(_native.batch_workspace_bytes(dcode, w, m, b, h, wc), "batch")
     upd_probe = int(bool(config.update_probe_modes) and config.alpha_probe > 0)
+    # every batch's position list for this rank: the whole batch in visit
+    # order (one rank) or this rank's spatial share (partition.py)
+    plan, lists = [], []
     if world > 1:
-        # canvas rows a batch can touch (union over ALL its positions, so the
-        # band is identical on every rank): only that band of the object
-        # accumulator is all-reduced -- the rest is zero on every rank
+        # anchor rows are fixed for the sweep (engine.py:193, 226-233): one
+        # small device-to-host read of the positions per sweep
         rows_h = np.rint(st.positions[:, 1].cpu().numpy()).astype(np.int64) - st.canvas_origin[0]
+    off = 0
     for s in range(0, n, b):
-        nb = min(b, n - s)
-        lo, hi = batch_slice(nb, rank, world)
-        if hi > lo:
-            args = _native.PtyBatchArgs(
-                dcode, w, m, n, _native.ptr(st.obj), h, wc, st.canvas_origin[0], st.canvas_origin[1],
-                _native.ptr(st.probe_stack), _native.ptr(pats), _native.ptr(pats_t), _native.ptr(st.positions),
-                _native.ptr(order_d) + 4 * (s + lo), hi - lo, s + lo,
-                float(config.alpha_obj), float(config.alpha_probe), float(config.beta),
-                float(config.gamma), float(config.epsilon_rel), upd_probe,
-                int(bool(config.track_modulus_error)), sense, _native.ptr(stage),
-                _native.ptr(obj_acc), _native.ptr(probe_acc), _native.ptr(err_part),
-                _native.ptr(status), _native.ptr(ws), ws.numel())
-            _native.batch_contrib(args)
+        ids = order[s:s + b]
+        if world == 1:
+            mine, first, owns, xf = ids, 0, None, None
+        else:
+            rows = rows_h[ids]
+            shares = rank_shares(rows, world)
+            bands = row_bands(rows, shares, w, h)
+            owns = ownership(bands)
+            xf = halo_transfers(bands, owns)
+            mine = ids[shares[rank]]
+            first = sum(len(shares[q]) for q in range(rank))   # distinct err_part rows per rank
+        plan.append((off, len(mine), s + first, owns, xf))
+        lists.append(np.asarray(mine, np.int32))
+        off += len(mine)
+    mine_all = np.concatenate(lists) if lists else np.zeros(0, np.int32)
+    lst_h = st.buffer("batch_list", (max(1, n),), t.int32, pinned=True)
+    lst_h.numpy()[:len(mine_all)] = mine_all
+    lst_d = st.buffer("batch_list", (max(1, n),), t.int32)
+    lst_d.copy_(lst_h, non_blocking=True)
+
+    def args_for(k0, count, visit0, sense_k):
+        return _native.PtyBatchArgs(
+            dcode, w, m, n, _native.ptr(st.obj), h, wc, st.canvas_origin[0], st.canvas_origin[1],
+            _native.ptr(st.probe_stack), _native.ptr(pats), _native.ptr(pats_t), _native.ptr(st.positions),
+            _native.ptr(lst_d) + 4 * k0, count, visit0,
+            float(config.alpha_obj), float(config.alpha_probe), float(config.beta),
+            float(config.gamma), float(config.epsilon_rel), upd_probe,
+            int(bool(config.track_modulus_error)), sense_k, _native.ptr(stage),
+            _native.ptr(obj_acc), _native.ptr(probe_acc), _native.ptr(err_part),
+            _native.ptr(status), _native.ptr(ws), ws.numel())
+
+    for k0, count, visit0, owns, xf in plan:
+        if count > 0:
+            _native.batch_contrib(args_for(k0, count, visit0, sense))
         else:
             obj_acc.zero_()
             probe_acc.zero_()
         if world > 1:
             import torch.distributed as dist
-            rb = rows_h[order[s:s + nb]]
-            r_lo, r_hi = max(0, int(rb.min())), min(h, int(rb.max()) + w)
-            for plane in range(3):
-                dist.all_reduce(obj_acc[plane, r_lo:r_hi], group=group)
+            _exchange_object_terms(obj_acc, owns, xf, rank, world, group)
             dist.all_reduce(probe_acc, group=group)
-        args = _native.PtyBatchArgs(
-            dcode, w, m, n, _native.ptr(st.obj), h, wc, st.canvas_origin[0], st.canvas_origin[1],
-            _native.ptr(st.probe_stack), _native.ptr(pats), _native.ptr(pats_t), _native.ptr(st.positions),
-            _native.ptr(order_d) + 4 * (s + min(lo, nb - 1)), max(hi - lo, 1), s + min(lo, nb - 1),
-            float(config.alpha_obj), float(config.alpha_probe), float(config.beta),
-            float(config.gamma), float(config.epsilon_rel), upd_probe,
-            int(bool(config.track_modulus_error)),
-            sense if hi > lo else _native.SENSE_NONE,        # stage o'_j only for this rank's positions
-            _native.ptr(stage), _native.ptr(obj_acc), _native.ptr(probe_acc), _native.ptr(err_part),
-            _native.ptr(status), _native.ptr(ws), ws.numel())
-        _native.batch_apply(args)
+        # every rank applies the same (complete) terms; the XCORR_A staging is
+        # only written for this rank's own positions
+        _native.batch_apply(args_for(k0 if count > 0 else 0, max(count, 1), visit0,
+                                     sense if count > 0 else _native.SENSE_NONE))
+    _native.batch_finalize(err_part, n, w, err)        # this rank's visits (the other rows are zero)
     if world > 1:
         import torch.distributed as dist
-        dist.all_reduce(err_part, group=group)
+        sums = err[:2].clone()
+        dist.all_reduce(sums, group=group)
+        worst = err[2:].clone()
+        dist.all_reduce(worst, op=dist.ReduceOp.MAX, group=group)
+        err[:2].copy_(sums)
+        err[2:].copy_(worst)
         # per-bit MAX (a MAX of the bitmasks would drop bits: 1 | 4 -> 4)
         bits = ((status >> t.arange(10, device=status.device, dtype=t.int32)) & 1).to(t.int32)
         dist.all_reduce(bits, op=dist.ReduceOp.MAX, group=group)
         status.copy_((bits << t.arange(10, device=status.device, dtype=t.int32)).sum().view(1))
-    _native.batch_finalize(err_part, n, w, err)
     if engaged and world == 1:
         _refine_positions(st, config.posref, n, w)
     elif engaged:
-        # every rank staged (o_j, o'_j) for its own slice of each batch; it
+        # every rank staged (o_j, o'_j) for its own share of each batch; it
         # senses and Adam-steps exactly those positions, then the disjoint
-        # updates are merged with a masked sum (x + 0 is exact) so positions
-        # and Adam state stay identical on every rank
-        mine = np.concatenate([order[s + batch_slice(min(b, n - s), rank, world)[0]:
-                                     s + batch_slice(min(b, n - s), rank, world)[1]]
-                               for s in range(0, n, b)]).astype(np.int32)
-        _refine_positions(st, config.posref, n, w, index=mine)
+        # updates are merged with ONE masked-sum all-reduce of (positions, m,
+        # v, t) (x + 0 is exact) so every rank holds the same state
+        _refine_positions(st, config.posref, n, w, index=mine_all)
         import torch.distributed as dist
-        mask = t.zeros((n,), dtype=t.bool, device=st.positions.device)
-        mask[t.from_numpy(mine).to(mask.device, t.int64)] = True
         ad = st.adam
-        for buf in (st.positions, ad.m, ad.v, ad.t):
-            part = t.where(mask.view(-1, *([1] * (buf.dim() - 1))), buf, t.zeros_like(buf))
-            dist.all_reduce(part, group=group)
-            buf.copy_(part)
+        mask = t.zeros((n, 1), dtype=t.float64, device=st.positions.device)
+        mask[t.from_numpy(mine_all.astype(np.int64)).to(mask.device)] = 1.0
+        packed = t.cat([st.positions, ad.m, ad.v, ad.t.to(t.float64).view(-1, 1)], dim=1) * mask
+        dist.all_reduce(packed, group=group)
+        st.positions.copy_(packed[:, 0:2])
+        ad.m.copy_(packed[:, 2:4])
+        ad.v.copy_(packed[:, 4:6])
+        ad.t.copy_(packed[:, 6].round().to(t.int64))
     if (config.ortho_interval > 0 and m > 1 and (st.iteration + 1) % config.ortho_interval == 0):
         _native.orthogonalize(st.probe_stack)
     he = st.buffer("err", (3,), t.float64, pinned=True)

@@ -1,8 +1,11 @@
 """Multi-rank decomposition of the batched extension, on CPU with gloo
-(world_size 2): every rank computes the update terms of its contiguous share
-of each batch (engine.batch_slice), the terms are all-reduced (sum) and every
-rank applies them -- the same steps engine.sweep_batched runs with NCCL.  The
-result must equal the single-rank batched sweep (oracle/batched.py)."""
+(world_size 2): every batch is split spatially (paper_2205_04295_b200/
+partition.py -- the same host logic engine.sweep_batched runs with NCCL):
+each rank computes the update terms of its row-sorted share, halo rows are
+sent point-to-point to their owner, which adds them in rank order, the owned
+rows are all-gathered and the probe terms all-reduced; every rank applies the
+identical update.  The result must equal the single-rank batched sweep
+(oracle/batched.py)."""
 
 import os
 import socket
@@ -15,7 +18,8 @@ import torch.multiprocessing as mp
 
 from conftest import golden
 from oracle import batched, rpie
-from paper_2205_04295_b200.engine import batch_slice
+from paper_2205_04295_b200.partition import (batch_slice, halo_transfers, ownership, rank_shares,
+                                             row_bands)
 from test_oracle_golden import cfg_from_repr
 
 
@@ -25,16 +29,39 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _allreduce_complex(a):
+def _allreduce(a):
     t = torch.from_numpy(np.ascontiguousarray(a).view(np.float64).copy())
     dist.all_reduce(t)
-    return t.numpy().view(np.complex128).reshape(a.shape)
+    return t.numpy().view(a.dtype).reshape(a.shape)
 
 
-def _allreduce_real(a):
-    t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64).copy())
-    dist.all_reduce(t)
-    return t.numpy()
+def _exchange_rows(acc, owns, xfers, rank, world):
+    """partition.py exchange on a (rows, cols) float64 accumulator."""
+    ops, recvs = [], []
+    for src, dst, a, b in xfers:
+        if src == rank:
+            ops.append(dist.P2POp(dist.isend, torch.from_numpy(acc[a:b].copy()), dst))
+        elif dst == rank:
+            buf = torch.empty((b - a, acc.shape[1]), dtype=torch.float64)
+            ops.append(dist.P2POp(dist.irecv, buf, src))
+            recvs.append((a, b, buf))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    for a, b, buf in recvs:
+        acc[a:b] += buf.numpy()
+    R = max(hi - lo for lo, hi in owns)
+    if R == 0:
+        return acc
+    lo, hi = owns[rank]
+    send = torch.zeros((R, acc.shape[1]), dtype=torch.float64)
+    send[:hi - lo] = torch.from_numpy(acc[lo:hi])
+    parts = [torch.empty_like(send) for _ in range(world)]
+    dist.all_gather(parts, send)
+    for q, (qlo, qhi) in enumerate(owns):
+        if q != rank and qhi > qlo:
+            acc[qlo:qhi] = parts[q][:qhi - qlo].numpy()
+    return acc
 
 
 def _worker(rank, world, port, batch, out_q):
@@ -46,18 +73,27 @@ def _worker(rank, world, port, batch, out_q):
     w = int(g["window"])
     pats = g["patterns"].astype(np.float64)
     st = rpie.initialize(pats, g["positions_in"], w, cfg)
+    h, wc = st.obj.shape
     for _ in range(2):
         order = rpie.visit_order(len(pats), cfg.position_order, cfg.shuffle_seed, st.iteration)
+        rows_all = np.array([rpie.anchor(p)[0] for p in st.positions]) - st.canvas_origin[0]
         num = den = 0.0
         for s in range(0, len(pats), batch):
             ids = order[s:s + batch]
-            lo, hi = batch_slice(len(ids), rank, world)
-            t = batched.contrib(st, pats, w, cfg, ids[lo:hi])
-            t.onum = _allreduce_complex(t.onum)
-            t.oden = _allreduce_real(t.oden)
-            t.pnum = [_allreduce_complex(p) for p in t.pnum]
-            t.pden = _allreduce_real(t.pden)
-            e = _allreduce_real(np.array([t.err_num, t.err_den]))
+            rows = rows_all[ids]
+            shares = rank_shares(rows, world)
+            bands = row_bands(rows, shares, w, h)
+            owns = ownership(bands)
+            xf = halo_transfers(bands, owns)
+            t = batched.contrib(st, pats, w, cfg, ids[shares[rank]])
+            # the object terms as [row][re, im, den][col] (the engine's layout)
+            acc = np.stack([t.onum.real, t.onum.imag, t.oden], axis=1).reshape(h, 3 * wc)
+            acc = _exchange_rows(acc, owns, xf, rank, world).reshape(h, 3, wc)
+            t.onum = acc[:, 0] + 1j * acc[:, 1]
+            t.oden = acc[:, 2].copy()
+            t.pnum = [_allreduce(p) for p in t.pnum]
+            t.pden = _allreduce(t.pden)
+            e = _allreduce(np.array([t.err_num, t.err_den]))
             num += e[0]
             den += e[1]
             batched.apply(st, cfg, t)
@@ -90,6 +126,32 @@ def test_two_rank_batched_sweep_equals_single_rank(batch):
     np.testing.assert_allclose(obj, ref.obj, rtol=0, atol=1e-13)
     np.testing.assert_allclose(probes, np.stack(ref.probes), rtol=0, atol=1e-13)
     np.testing.assert_allclose(trace, ref.error_trace, rtol=1e-12)
+
+
+def test_spatial_partition_covers_every_row_once():
+    """rank_shares / row_bands / ownership / halo_transfers: every batch
+    position is on exactly one rank, the owned ranges tile the batch's band,
+    and every accumulator row a rank computed either is its own or is sent to
+    the one rank that owns it."""
+    rng = np.random.default_rng(0)
+    for world in (1, 2, 3, 4, 8):
+        for n in (1, 3, 40, 400):
+            rows = rng.integers(0, 500, n)
+            shares = rank_shares(rows, world)
+            assert sorted(np.concatenate(shares).tolist()) == list(range(n))
+            bands = row_bands(rows, shares, 64, 600)
+            owns = ownership(bands)
+            xf = halo_transfers(bands, owns)
+            live = [o for o in owns if o[1] > o[0]]
+            assert live[0][0] == int(rows.min()) and live[-1][1] == min(600, int(rows.max()) + 64)
+            for (a, b), (c, d) in zip(live, live[1:]):
+                assert b == c
+            for r, (lo, hi) in enumerate(bands):
+                for row in range(lo, hi):
+                    owner = [q for q, (olo, ohi) in enumerate(owns) if olo <= row < ohi]
+                    assert len(owner) == 1
+                    if owner[0] != r:
+                        assert any(src == r and dst == owner[0] and a <= row < b for src, dst, a, b in xf)
 
 
 def test_batch_slices_partition_the_batch():

@@ -2,7 +2,9 @@
 on ONE GPU: two processes share the device, each runs its share of every batch
 through the CUDA kernels and the update terms are all-reduced with gloo (host
 copies; no kernel waits on another).  Result == the single-process batched
-sweep of the same batches (the NCCL path on 2-8 GPUs runs the same code)."""
+sweep of the same batches (the NCCL path on 2-8 GPUs runs the same code:
+spatial shares, halo rows to their owner, owned rows all-gathered,
+partition.py)."""
 
 import os
 import socket
@@ -72,3 +74,14 @@ def test_two_rank_batched_sweep_matches_one_rank(gpu, name):
         if one[5] is not None:
             np.testing.assert_array_equal(two[5], one[5])
     np.testing.assert_array_equal(twos[0][4], twos[1][4])
+
+
+def test_two_rank_batched_sweep_reruns_bitwise(gpu):
+    """The 2-rank decomposition is deterministic: two runs are bit-identical
+    (fixed shares, fixed halo order, fixed reduction order)."""
+    a = _spawn(2, "posref_a")
+    b = _spawn(2, "posref_a")
+    for x, y in zip(a, b):
+        assert np.array_equal(x[1], y[1]) and np.array_equal(x[2], y[2])
+        assert x[3] == y[3]
+        assert np.array_equal(x[4], y[4])

@@ -1,0 +1,10 @@
+set -o pipefail
+mkdir -p gpurun_out
+for pair in 0 1; do
+echo "== pair $pair"
+PTY_SLOT_PAIR=$pair PTY_SWEEP_TILES_MAX=0 PTY_TIMELINE=60 timeout -s KILL 300 python tools/tl_phases.py 18 3 2>&1 | tail -7
+done
+timeout -s KILL 1500 python -m pytest tests -m gpu -q -x --timeout 600 > gpurun_out/r2h_tests.log 2>&1; echo "tests rc=$?"
+tail -3 gpurun_out/r2h_tests.log
+timeout -s KILL 900 python bench.py --steps 6 --warmup 3 --no-cpu --no-batched --no-configs --no-fp64 > gpurun_out/r2h_bench.json 2> gpurun_out/r2h_bench.err; echo "bench rc=$?"
+python -c "import json;d=json.loads(open('gpurun_out/r2h_bench.json').read().strip().splitlines()[-1]);print(d['value'],d['roofline']['frac'],d['e2e']['value'])"
