@@ -326,25 +326,28 @@ def e2e_arm(args, states, dsets, cfgs, dev, world):
     R = len(states)
     hosts = [torch.from_numpy(np.ascontiguousarray(d.patterns, np.float32)).pin_memory() for d in dsets]
     dxs = [pk.PtychoDataset(patterns=d.patterns, positions=d.positions, geometry=d.geometry) for d in dsets]
-    dev_pat = [pk.engine.device_patterns(x, torch.float32) for x in dxs]
-    dev_pat_t = [pk.engine.device_patterns_t(x, torch.float32) for x in dxs]
-    # the H2D of step i+1 runs on a copy stream (copy engines, no SMs) while
-    # step i sweeps: two pinned-to-device staging sets, event-ordered; each
-    # step then moves its staged inputs into the datasets' device buffers
+    for x in dxs:                                           # the datasets' device buffers exist (validated once)
+        pk.engine.device_patterns_t(x, torch.float32)
+    # every step's H2D lands directly in one of two raw device buffer sets (copy
+    # stream, copy engines) while the previous step sweeps; the step then lays
+    # out its transposed copy (the column passes' layout) and points the
+    # datasets at its buffers -- no device-to-device staging copy
     main = torch.cuda.current_stream()
     cstream = torch.cuda.Stream()
-    stage = [[torch.empty_like(p) for p in dev_pat] for _ in range(2)]
+    raw = [[torch.empty(h.shape, dtype=torch.float32, device=dev) for h in hosts] for _ in range(2)]
+    pt = [torch.empty(h.shape, dtype=torch.float32, device=dev) for h in hosts]
     copied = [torch.cuda.Event() for _ in range(2)]
     consumed = [torch.cuda.Event() for _ in range(2)]
     used = [False, False]
+    key = str(torch.float32)
 
     def issue_copy(i):
         slot = i % 2
         if used[slot]:
             cstream.wait_event(consumed[slot])
         with torch.cuda.stream(cstream):
-            for st_, h in zip(stage[slot], hosts):
-                st_.copy_(h, non_blocking=True)                      # H2D: step i's inputs
+            for d_, h in zip(raw[slot], hosts):
+                d_.copy_(h, non_blocking=True)                       # H2D: step i's inputs
             copied[slot].record(cstream)
 
     def run_steps(n):
@@ -354,9 +357,10 @@ def e2e_arm(args, states, dsets, cfgs, dev, world):
             main.wait_event(copied[slot])
             if i + 1 < n:
                 issue_copy(i + 1)
-            for r in range(R):
-                dev_pat[r].copy_(stage[slot][r])
-                dev_pat_t[r].copy_(stage[slot][r].transpose(1, 2))  # device re-layout
+            for r, x in enumerate(dxs):
+                pt[r].copy_(raw[slot][r].transpose(1, 2))             # device re-layout
+                x._device[(key, id(x.patterns))] = raw[slot][r]
+                x._device[("T", key, id(x.patterns))] = pt[r]
             consumed[slot].record(main)
             used[slot] = True
             pk.sweep_replicas(states, dxs, cfgs)                     # ends with the D2H of the metric

@@ -157,6 +157,16 @@ __device__ __forceinline__ T task_row_fwd_staged(const cplx<T>* tw, cplx<T>* lin
 #pragma unroll
     for (int a = 0; a < A; ++a) ov[a] = orow[B * a + b];
 #else
+#ifdef PTY_P1_CPASYNC
+    // modes >= 1: probe rows straight into their (still unpadded) lines
+#pragma unroll
+    for (int m = 1; m < MODES; ++m)
+#pragma unroll
+        for (int i = 0; i < W / (2 * B); ++i) {
+            const int q = b + B * i;
+            cp_async<16>(lines + (m * 4 + gi) * LS4 + 2 * q, prow + m * WW + 2 * q);
+        }
+#endif
     C ov[A], pv[A];
 #pragma unroll
     for (int a = 0; a < A; ++a) {
@@ -181,6 +191,23 @@ __device__ __forceinline__ T task_row_fwd_staged(const cplx<T>* tw, cplx<T>* lin
 #pragma unroll
         for (int a = 0; a < A; ++a) pv[a] = line[B * a + b];          // P_m row, contiguous
         __syncwarp(gmask);
+#pragma unroll
+        for (int a = 0; a < A; ++a) {
+            const int n = B * a + b;
+            line[pad<W>(n)] = scale(pv[a] * ov[a], checker<T>(r, n));
+        }
+    }
+#elif defined(PTY_P1_CPASYNC)
+    cp_async_wait_all();
+    __syncwarp(gmask);
+#pragma unroll
+    for (int m = 0; m < MODES; ++m) {
+        C* line = lines + (m * 4 + gi) * LS4;
+        if (m > 0) {
+#pragma unroll
+            for (int a = 0; a < A; ++a) pv[a] = line[B * a + b];
+            __syncwarp(gmask);
+        }
 #pragma unroll
         for (int a = 0; a < A; ++a) {
             const int n = B * a + b;
@@ -250,8 +277,34 @@ __device__ __forceinline__ T task_col_fwd(const cplx<T>* tw, cplx<T>* xch, int b
         *mphase ^= 1u;
     }
 #endif
+#if defined(PTY_P2_PREFETCH) && !defined(PTY_TMA_LINES)
+    C nxt[A];
+    if constexpr (RES) {
+#pragma unroll
+        for (int a = 0; a < A; ++a) nxt[a] = pos[(size_t)kc * W + B * a + b];
+    }
+#endif
     for (int m = 0; m < M;++m) {
         C* line = pos + m * WW + (size_t)kc * W;
+#if defined(PTY_P2_PREFETCH) && !defined(PTY_TMA_LINES)
+        if constexpr (RES) {   // mode m+1's column loads fly during mode m's transform
+            C cur[A];
+#pragma unroll
+            for (int a = 0; a < A; ++a) cur[a] = nxt[a];
+            if (m + 1 < M) {
+#pragma unroll
+                for (int a = 0; a < A; ++a) nxt[a] = line[WW + B * a + b];
+            }
+            C* rl = res + m * xch_size<W>();
+            group_fft<T, W, false>(
+                rl, tw, b, gmask, [&](int, int a) { return cur[a]; },
+                [&](int u, int slot, C v) {
+                    rl[pad<W>(u)] = v;
+                    tot[slot] += norm2(v) * invW2;
+                });
+            continue;
+        }
+#endif
         if constexpr (RES) {   // Psi_m stays in this group's shared-memory line for P3
             C* rl = res + m * xch_size<W>();
             group_fft<T, W, false>(

@@ -504,7 +504,7 @@ def sweep_batched(state: ReconState, dataset, config: SolverConfig, group=None) 
             dist.all_reduce(probe_acc, group=group)
         # every rank applies the same (complete) terms; the XCORR_A staging is
         # only written for this rank's own positions
-        _native.batch_apply(args_for(k0 if count > 0 else 0, max(count, 1), visit0,
+        _native.batch_apply(args_for(k0 if count > 0 else 0, max(count, 1), min(visit0, n - 1),
                                      sense if count > 0 else _native.SENSE_NONE))
     _native.batch_finalize(err_part, n, w, err)        # this rank's visits (the other rows are zero)
     if world > 1:
