@@ -642,12 +642,20 @@ def sweep_replicas(states, datasets, config: SolverConfig, orders=None, kernel_e
             if it not in perms:
                 perms[it] = visit_order(n, config, it)
             rb["order_h"].numpy()[k] = perms[it]
-    rb["order_d"].copy_(rb["order_h"], non_blocking=True)
+    # throughput sweeps (line-task kernel, > 4 replicas) read the visit orders
+    # straight from the pinned host buffer (unified addressing; phase 0 turns
+    # them into the device step table): no host-to-device copy on the stream,
+    # so a sweep never queues behind a bulk upload occupying the copy engine
+    # (e.g. the next step's diffraction data).  The latency kernel (<= 4
+    # replicas) reads the order every step and gets a device copy.
+    host_order = R > 4 and not config.subpixel_gather
+    if not host_order:
+        rb["order_d"].copy_(rb["order_h"], non_blocking=True)
     rb["status_d"].zero_()
     for k, (st, ds) in enumerate(zip(states, datasets)):
         pats = device_patterns(ds, rdt)
         pats_t = device_patterns_t(ds, rdt)
-        order_d = rb["order_d"][k]
+        order_d = rb["order_h"][k] if host_order else rb["order_d"][k]
         status = rb["status_d"][k:k + 1]
         err = rb["err_d"][k]
         stage = st.buffer("stage", (n, 2, w, w), cdt) if sense != _native.SENSE_NONE else None
