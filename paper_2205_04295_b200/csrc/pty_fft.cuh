@@ -25,7 +25,13 @@ template <> struct Shape<16>   { static constexpr int A = 4,  B = 4;  };
 template <> struct Shape<32>   { static constexpr int A = 8,  B = 4;  };
 template <> struct Shape<64>   { static constexpr int A = 8,  B = 8;  };
 template <> struct Shape<128>  { static constexpr int A = 16, B = 8;  };
+#ifdef PTY_NARROW256
+// narrow W = 256 lines (pty_sweep_f32_w256n.cu, compiled in namespace pty_n):
+// a whole warp per line, 8 points per thread, 256 = 8 x 8 x 4 (group_fft below)
+template <> struct Shape<256>  { static constexpr int A = 8, B = 32; };
+#else
 template <> struct Shape<256>  { static constexpr int A = 16, B = 16; };
+#endif
 template <> struct Shape<512>  { static constexpr int A = 32, B = 16; };
 
 template <int N> struct Log2 { static constexpr int value = 1 + Log2<N / 2>::value; };
@@ -122,7 +128,7 @@ __device__ __forceinline__ void load_twiddles(cplx<T>* tw_smem, const cplx<T>* t
 template <typename T, int W, bool INV>
 __device__ __forceinline__ void apply_twiddles(cplx<T>* v, const cplx<T>* tw, int b) {
     constexpr int A = Shape<W>::A, B = Shape<W>::B;
-    if constexpr (std::is_same<T, float>::value && A >= 8) {
+    if constexpr (std::is_same<T, float>::value && A >= 8 && A >= B) {
         cplx<T> wr[4], wq[A / 4];
         wr[0] = cplx<T>{T(1), T(0)};
         wq[0] = cplx<T>{T(1), T(0)};
@@ -145,11 +151,70 @@ __device__ __forceinline__ void apply_twiddles(cplx<T>* v, const cplx<T>* tw, in
     }
 }
 
+// Narrow line DFT (A = 8 points per lane, B = 32 lanes, W = 256 = 8 x 8 x 4),
+// used when A < B.  Lane b holds x[32a + b]; stage 1 is a DFT8 over a with
+// the inter-stage twiddles w256^(b k1); the DFT32 over b that remains for
+// every k1 is split as b = 4c + d, k2 = e + 8f:
+//   X[k1 + 8e + 64f] = sum_d w4^(df) w32^(de) sum_c Y_{4c+d}[k1] w8^(ce),
+// stage 2a = DFT8 over c on lane (k1 = b/4, d = b%4) after exchange 1,
+// twiddle w32^(de) = tw[e*32 + 8d], stage 2b = DFT4 over d on lane
+// (k1, d2) for e in {2 d2, 2 d2 + 1} after exchange 2.  Both exchanges use a
+// 256-slot XOR-swizzled layout that is bank-conflict free for 8-byte values
+// on writes and reads.  Lane (k1, d2) outputs k = k1 + 8(2 d2 + p) + 64 f at
+// slot p*4 + f.
+template <typename T, bool INV, typename LD, typename ST>
+__device__ __forceinline__ void narrow_fft256(cplx<T>* xch, const cplx<T>* tw, int b, unsigned mask, LD&& load,
+                                              ST&& store) {
+    constexpr int B = 32;
+    cplx<T> v[8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) v[a] = load(B * a + b, a);
+    DFT<T, 8, INV>::run(v);
+    apply_twiddles<T, 256, INV>(v, tw, b);
+    __syncwarp(mask);
+#pragma unroll
+    for (int k1 = 0; k1 < 8; ++k1) xch[32 * k1 + (b ^ (4 * k1))] = v[k1];
+    __syncwarp(mask);
+    const int k1s = b >> 2, d = b & 3, sw = 4 * (k1s & 3);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) v[c] = xch[32 * k1s + ((4 * c + d) ^ (4 * k1s))];
+    __syncwarp(mask);
+    DFT<T, 8, INV>::run(v);
+#pragma unroll
+    for (int e = 1; e < 8; ++e) {
+        const cplx<T> w = tw[e * 32 + 8 * d];                  // w32^(d e) = w256^(8 d e)
+        v[e] = INV ? mulc(v[e], w) : v[e] * w;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) xch[32 * k1s + ((4 * e + ((d + (e >> 1)) & 3)) ^ sw)] = v[e];
+    __syncwarp(mask);
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[p * 4 + q] = xch[32 * k1s + ((4 * (2 * d + p) + ((q + d) & 3)) ^ sw)];
+    __syncwarp(mask);
+    DFT<T, 4, INV>::run(&v[0]);
+    DFT<T, 4, INV>::run(&v[4]);
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int f = 0; f < 4; ++f) store(k1s + 8 * (2 * d + p) + 64 * f, p * 4 + f, v[p * 4 + f]);
+}
+
 // Transform one padded line in shared memory with a group of B threads.
 // b = thread index in the group, mask = the group's lanes.
 template <typename T, int W, bool INV>
 __device__ __forceinline__ void line_fft(cplx<T>* line, const cplx<T>* tw, int b, unsigned mask) {
-    constexpr int A = Shape<W>::A, B = Shape<W>::B, Q = A / B;
+    constexpr int A = Shape<W>::A, B = Shape<W>::B;
+    if constexpr (A < B) {
+        static_assert(W == 256 && A == 8 && B == 32, "narrow lines: W = 256 only");
+        narrow_fft256<T, INV>(
+            line, tw, b, mask, [&](int n, int) { return line[n + n / B]; },
+            [&](int k, int, cplx<T> x) { line[k + k / B] = x; });
+        __syncwarp(mask);
+        return;
+    } else {
+    constexpr int Q = A / B;
     cplx<T> v[A];
 #pragma unroll
     for (int a = 0; a < A; ++a) v[a] = line[a * (B + 1) + b];
@@ -174,6 +239,7 @@ __device__ __forceinline__ void line_fft(cplx<T>* line, const cplx<T>* tw, int b
         }
     }
     __syncwarp(mask);
+    }
 }
 
 // Fused-I/O line FFT by a group of B threads.  Stage 1 takes its A inputs from
@@ -186,7 +252,13 @@ __device__ __forceinline__ void line_fft(cplx<T>* line, const cplx<T>* tw, int b
 template <typename T, int W, bool INV, typename LD, typename ST>
 __device__ __forceinline__ void group_fft(cplx<T>* xch, const cplx<T>* tw, int b, unsigned mask, LD&& load,
                                           ST&& store) {
-    constexpr int A = Shape<W>::A, B = Shape<W>::B, Q = A / B;
+    constexpr int A = Shape<W>::A, B = Shape<W>::B;
+    if constexpr (A < B) {
+        static_assert(W == 256 && A == 8 && B == 32, "narrow lines: W = 256 only");
+        narrow_fft256<T, INV>(xch, tw, b, mask, load, store);
+        return;
+    } else {
+    constexpr int Q = A / B;
     cplx<T> v[A];
 #pragma unroll
     for (int a = 0; a < A; ++a) v[a] = load(B * a + b, a);
@@ -206,6 +278,7 @@ __device__ __forceinline__ void group_fft(cplx<T>* xch, const cplx<T>* tw, int b
         DFT<T, B, INV>::run(&v[i * B]);
 #pragma unroll
         for (int k2 = 0; k2 < B; ++k2) store(b + B * i + A * k2, i * B + k2, v[i * B + k2]);
+    }
     }
 }
 

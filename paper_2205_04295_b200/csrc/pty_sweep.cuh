@@ -22,7 +22,11 @@
 
 namespace pty {
 
+#ifdef PTY_NARROW256
+constexpr int kSweepThreads = 512;     // narrow W = 256 lines: 32-lane groups, 128-thread teams
+#else
 constexpr int kSweepThreads = 256;
+#endif
 constexpr int kSweepMaxCtasPerSm = 2;
 constexpr int kMaxSlots = 24;
 constexpr int kMaxModes = 8;

@@ -59,12 +59,24 @@ inline size_t sweep_workspace(int W, int M, int N, int S) {
 template <typename T, int W>
 int run_sweep_lines(const PtySweepArgs* a, cudaStream_t st);
 
+}  // namespace pty
+// the narrow-line fp32 W = 256 build (pty_sweep_f32_w256n.cu)
+extern "C" int pty_internal_sweep_narrow_f32_w256(const PtySweepArgs* a, void* stream);
+namespace pty {
+
+inline bool narrow_lines() { return env_int("PTY_NARROW", 0) != 0; }
+
 template <typename T, int W>
 int run_sweep(const PtySweepArgs* a, cudaStream_t st) {
     if (a->n_slots <= tiles_max_slots()) {
         const int rc = tiles::run_sweep<T, W>(a, st);
         if (rc != tiles::kTilesNoFit) return rc;
     }
+#ifdef PTY_BUILD_NARROW
+    if constexpr (std::is_same<T, float>::value && W == 256) {
+        if (narrow_lines()) return pty_internal_sweep_narrow_f32_w256(a, st);
+    }
+#endif
     return run_sweep_lines<T, W>(a, st);
 }
 

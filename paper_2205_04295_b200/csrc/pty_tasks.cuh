@@ -63,7 +63,10 @@ template <int W> __host__ __device__ constexpr int acc_stride() { return W + 16;
 // output column of stage-2 slot q for group lane b
 template <int W> __device__ __forceinline__ int slot_col(int b, int q) {
     constexpr int A = Shape<W>::A, B = Shape<W>::B;
-    return b + B * (q / B) + A * (q % B);
+    if constexpr (A < B)                       // narrow_fft256: lane (k1, d2), slot p*4 + f
+        return (b >> 2) + 8 * (2 * (b & 3) + (q >> 2)) + 64 * (q & 3);
+    else
+        return b + B * (q / B) + A * (q % B);
 }
 
 // Team-level max of one value per group (4 groups); red4 = 4 shared slots of the team.
