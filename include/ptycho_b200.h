@@ -138,8 +138,10 @@ PTY_API int pty_fft2(void* data, int32_t dtype, int32_t window, int32_t batch, i
 /*
  * Batched registration (registration.py:123-128) of n pairs.
  * work: [n][2][W][W] complex; plane 0 = reference, plane 1 = moving on entry
- *       (overwritten).  If real_inputs != 0, ref_real/mov_real ([n][W][W] real)
- *       are loaded instead and `work` is only scratch.
+ *       (overwritten).  real_inputs = 1: ref_real/mov_real ([n][W][W] real)
+ *       are loaded instead and `work` is only scratch; real_inputs = 2 (dtype
+ *       C128 only): ref_real points at complex64 pairs [n][2][W][W] that are
+ *       widened to float64 while loading (fp32 states registered in float64).
  * weighting: 0 = "phase", 1 = "raw".  kappa in {1} U [2, 1000].
  * Outputs (device): dy, dx, peak [n] float64; ok [n] int32 (0 = degenerate spectrum).
  */

@@ -238,14 +238,18 @@ def sweep_workspace_bytes(dtype: int, window: int, modes: int, n: int, slots: in
 
 
 def register_batch(work, window: int, n: int, weighting: int, kappa: int, dy, dx, peak, ok,
-                   ref_real=None, mov_real=None) -> None:
+                   ref_real=None, mov_real=None, pairs_c64=None) -> None:
+    """pty_register_batch; ``pairs_c64`` (complex64 [n][2][W][W]) are widened to
+    the complex128 ``work`` while loading."""
     lib = load()
     sb = int(lib.pty_register_scratch_bytes(window, n, kappa))
     if sb < 0:
         raise NativeError("unsupported registration geometry")
     ws = workspace(sb, "register")
-    real = ref_real is not None
-    check(lib.pty_register_batch(ptr(work), ptr(ref_real), ptr(mov_real), int(real),
+    real = 2 if pairs_c64 is not None else int(ref_real is not None)
+    if pairs_c64 is not None:
+        ref_real = pairs_c64
+    check(lib.pty_register_batch(ptr(work), ptr(ref_real), ptr(mov_real), real,
                                  dtype_code(work), window, n, weighting, kappa,
                                  ptr(dy), ptr(dx), ptr(peak), ptr(ok), ptr(ws), ws.numel(),
                                  stream_ptr()), "pty_register_batch")

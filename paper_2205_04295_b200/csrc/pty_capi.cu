@@ -196,7 +196,7 @@ int pty_fft2(void* data, int32_t dtype, int32_t W, int32_t batch, int32_t invers
 int64_t pty_register_scratch_bytes(int32_t W, int32_t n, int32_t kappa) {
     if (!valid_window(W) || n < 0) return -1;
     const int npts = kappa <= 1 ? 1 : ((int)(1.5 * kappa) | 1);
-    const size_t nIB = (size_t)(npts + 7) / 8;
+    const size_t nIB = (size_t)(npts + 3) / 4;               // refine_rows() >= 4
     Carver c(nullptr);
     c.take<void>((size_t)n * W * sizeof(double));          // max|xps| partials (<= W col tiles)
     c.take<ArgPart>((size_t)n * W * sizeof(ArgPart));       // coarse partials
@@ -211,7 +211,9 @@ int pty_register_batch(void* work, const void* ref_real, const void* mov_real, i
     if (!work || !valid_window(W) || n < 0 || !dy || !dx || !peak || !ok) return PTY_ERR_ARGUMENT;
     if (!(kappa == 1 || (kappa >= 2 && kappa <= 1000))) return PTY_ERR_ARGUMENT;
     if (weighting != 0 && weighting != 1) return PTY_ERR_ARGUMENT;
-    if (real_inputs && (!ref_real || !mov_real)) return PTY_ERR_ARGUMENT;
+    if (real_inputs == 1 && (!ref_real || !mov_real)) return PTY_ERR_ARGUMENT;
+    if (real_inputs == 2 && (!ref_real || dtype != PTY_DTYPE_C128)) return PTY_ERR_ARGUMENT;
+    if (real_inputs < 0 || real_inputs > 2) return PTY_ERR_ARGUMENT;
     if (scratch_bytes < pty_register_scratch_bytes(W, n, kappa)) return PTY_ERR_ARGUMENT;
     if (n == 0) return PTY_OK;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -227,7 +229,7 @@ int pty_register_batch(void* work, const void* ref_real, const void* mov_real, i
             Carver c(scratch);
             T* mx = c.take<T>((size_t)n * WW * sizeof(double));
             ArgPart* cpart = c.take<ArgPart>((size_t)n * WW * sizeof(ArgPart));
-            RefPart* rpart = c.take<RefPart>((size_t)n * ((npts + 7) / 8) * sizeof(RefPart));
+            RefPart* rpart = c.take<RefPart>((size_t)n * ((npts + 3) / 4) * sizeof(RefPart));
             cplx<T>* wk = static_cast<cplx<T>*>(work);
             const size_t line = (size_t)line_stride<WW>() * sizeof(cplx<T>);
             const size_t fix = (size_t)WW * sizeof(cplx<T>) + 64 * sizeof(double);

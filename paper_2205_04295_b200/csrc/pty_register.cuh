@@ -22,8 +22,9 @@ namespace pty {
 
 constexpr int kRegThreads = 256;
 // rows of the upsampled grid per CTA (keeps 2 * rows * W complex in shared memory)
+// 64 KB of shared memory per CTA (several CTAs per SM): 4..16 rows
 template <typename T, int W> __host__ __device__ constexpr int refine_rows() {
-    return W * (int)sizeof(cplx<T>) >= 8192 ? 8 : 16;
+    return 32768 / (W * (int)sizeof(cplx<T>)) < 4 ? 4 : (32768 / (W * (int)sizeof(cplx<T>)) > 16 ? 16 : 32768 / (W * (int)sizeof(cplx<T>)));
 }
 template <typename T, int W> __host__ __device__ constexpr size_t refine_smem() {
     return (size_t)2 * refine_rows<T, W>() * W * sizeof(cplx<T>);
@@ -60,8 +61,14 @@ __global__ void __launch_bounds__(kRegThreads) reg_rows_fwd(cplx<T>* work, const
         const int pl = i / (TR * W), rem = i % (TR * W), r = rem / W, c = rem % W;
         const size_t off = (size_t)(rt * TR + r) * W + c;
         C v;
-        if (real_inputs) v = C{(pl ? mov_real : ref_real)[(size_t)pr * WW + off], T(0)};
-        else v = work[((size_t)pr * 2 + pl) * WW + off];
+        if (real_inputs == 2) {            // complex64 pairs [n][2][W][W] (ref_real), widened on load
+            const float2 x = reinterpret_cast<const float2*>(ref_real)[((size_t)pr * 2 + pl) * WW + off];
+            v = C{T(x.x), T(x.y)};
+        } else if (real_inputs) {
+            v = C{(pl ? mov_real : ref_real)[(size_t)pr * WW + off], T(0)};
+        } else {
+            v = work[((size_t)pr * 2 + pl) * WW + off];
+        }
         tile[(size_t)(pl * TR + r) * LS + pad<W>(c)] = v;
     }
     __syncthreads();
@@ -266,7 +273,8 @@ __global__ void __launch_bounds__(kRegThreads) reg_refine(const cplx<T>* work, i
     for (int q = 0; q < VPT; ++q)
 #pragma unroll
         for (int i = 0; i < kRefineRows; ++i) acc[q][i] = C{T(0), T(0)};
-    for (int u = 0; u < W; ++u) {
+#pragma unroll 4
+    for (int u = 0; u < W; ++u) {                              // 4 rows of xps in flight per thread
 #pragma unroll
         for (int q = 0; q < VPT; ++q) {
             const int v = threadIdx.x + q * kRegThreads;

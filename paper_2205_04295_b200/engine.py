@@ -727,14 +727,14 @@ def _refine_positions(st: ReconState, pc: PosRefConfig, n: int, w: int, index=No
     else:
         # register in float64 like the reference (its crops are complex128,
         # registration.py:123-128): fp32 correlation peaks of near-identical
-        # crops are too flat to resolve the 1/kappa grid
+        # crops are too flat to resolve the 1/kappa grid; the complex64 pairs
+        # are widened while the first kernel loads them (no conversion pass)
         chunk = max(1, min(n, (1 << 30) // (2 * w * w * 16)))
         work = st.buffer("stage64", (chunk, 2, w, w), t.complex128)
         for s in range(0, n, chunk):
             e = min(n, s + chunk)
-            work[:e - s].copy_(stage[s:e])
             _native.register_batch(work[:e - s], w, e - s, 1, int(pc.kappa),
-                                   dy[s:e], dx[s:e], peak[s:e], ok[s:e])
+                                   dy[s:e], dx[s:e], peak[s:e], ok[s:e], pairs_c64=stage[s:e])
     # sensors return (gx, gy) = (est.dx, est.dy) (posref.py:63)
     _native.adam_apply(st.positions, st.adam, dx, dy, ok, pc, position_bounds(st, w), index=idx_d)
 
