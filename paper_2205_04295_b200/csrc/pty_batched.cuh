@@ -114,7 +114,10 @@ constexpr int kLineThreads = 128;
 // K1: exit waves C * P_m * o_j and row DFTs (engine.py:113, fields.py:81).
 // Team task (k, m, row quad); output transposed into scratch.
 template <typename T, int W>
-__global__ void __launch_bounds__(kLineThreads) bk_rows_fwd(const __grid_constant__ BatchDev P) {
+#ifndef PTY_BK_ROWS_MINB
+#define PTY_BK_ROWS_MINB 4      // 128 registers: measured best (6 -> 85 registers spills: 242 K vs 294 K pos/s)
+#endif
+__global__ void __launch_bounds__(kLineThreads, PTY_BK_ROWS_MINB) bk_rows_fwd(const __grid_constant__ BatchDev P) {
     using C = cplx<T>;
     constexpr int B = Shape<W>::B, TEAM = 4 * B, NTEAM = kLineThreads / TEAM, XS = xch_size<W>();
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -208,7 +211,7 @@ __global__ void __launch_bounds__(kLineThreads) bk_cols_mod(const __grid_constan
 // probe numerator (and, for m = 0, the probe denominator) in shared memory --
 // a fixed-order, atomic-free reduction.
 template <typename T, int W>
-__global__ void bk_rows_inv(const __grid_constant__ BatchDev P) {
+__global__ void __launch_bounds__(64, 2 * PTY_BK_ROWS_MINB) bk_rows_inv(const __grid_constant__ BatchDev P) {
     using C = cplx<T>;
     constexpr int A = Shape<W>::A, B = Shape<W>::B, TEAM = 4 * B, LS4 = team_line_stride<W>();
     extern __shared__ __align__(16) unsigned char smem_raw[];

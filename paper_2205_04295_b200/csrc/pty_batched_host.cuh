@@ -17,11 +17,24 @@ struct BatchShape {
     int nRT, G, ntiles, chunk;
 };
 
-// Positions per chunk (PTY_BATCH_CHUNK overrides; default: the whole batch)
-inline int batch_chunk(int b) {
+// Positions per chunk (PTY_BATCH_CHUNK overrides).  Default: the whole batch,
+// capped by a device-memory budget for the per-position scratch and object
+// numerators (2 M W^2 complex each, PTY_BATCH_BUDGET_MB, default 8 GB) and by
+// the gather kernel's shared-memory position list (4 bytes per position), so
+// a large batch_size runs in chunks instead of failing.
+inline int batch_chunk(int b, size_t per_pos_bytes = 0) {
     const int c = env_int("PTY_BATCH_CHUNK", 0);
-    return c > 0 ? std::min(c, b) : b;
+    if (c > 0) return std::min(c, b);
+    int chunk = b;
+    if (per_pos_bytes > 0) {
+        const size_t budget = (size_t)std::max(1, env_int("PTY_BATCH_BUDGET_MB", 8192)) << 20;
+        chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)chunk, budget / per_pos_bytes));
+    }
+    const size_t smem = max_dyn_smem();
+    if (smem > 1024) chunk = std::min(chunk, (int)((smem - 1024) / sizeof(int)));
+    return std::max(1, chunk);
 }
+template <typename T> inline size_t batch_pos_bytes(int W, int M) { return (size_t)2 * M * W * W * sizeof(cplx<T>); }
 
 template <int W> inline int k4_groups(int chunk) {
     const int g = env_int("PTY_K4_GROUPS", 0);
@@ -30,9 +43,9 @@ template <int W> inline int k4_groups(int chunk) {
     return std::max(1, std::min(chunk, (want + W / 4 - 1) / (W / 4)));
 }
 
-inline BatchShape batch_shape(int W, int b, int H, int Wc, int G) {
+inline BatchShape batch_shape(int W, int b, int H, int Wc, int G, int chunk) {
     BatchShape s;
-    s.chunk = batch_chunk(b);
+    s.chunk = chunk;
     s.nRT = W / 4;                                            // pp_part: 4-row tiles
     s.G = G;
     s.ntiles = ((H + kObjTile - 1) / kObjTile) * ((Wc + kObjTile - 1) / kObjTile);
@@ -62,7 +75,8 @@ inline BatchLayout carve_batch(void* ws, int W, int M, int b, const BatchShape& 
 template <typename T, int W>
 int fill_batch(const PtyBatchArgs* a, BatchDev& P, BatchShape& sh, cudaStream_t st) {
     const int M = a->modes, b = a->n_batch;
-    sh = batch_shape(W, b, a->H, a->Wc, k4_groups<W>(batch_chunk(b)));
+    const int chunk = batch_chunk(b, batch_pos_bytes<T>(W, M));
+    sh = batch_shape(W, b, a->H, a->Wc, k4_groups<W>(chunk), chunk);
     const bool upd = a->sense == PTY_SENSE_XCORR_A;
     BatchLayout L = carve_batch<T>(a->workspace, W, M, b, sh, a->H, a->Wc, upd);
     if (!a->workspace || a->workspace_bytes < (int64_t)L.bytes) return PTY_ERR_ARGUMENT;
@@ -174,7 +188,8 @@ int run_batch_apply(const PtyBatchArgs* a, cudaStream_t st) {
 
 template <typename T, int W>
 int64_t batch_workspace(int M, int b, int H, int Wc, bool upd) {
-    BatchShape sh = batch_shape(W, b, H, Wc, k4_groups<W>(batch_chunk(b)));
+    const int chunk = batch_chunk(b, batch_pos_bytes<T>(W, M));
+    BatchShape sh = batch_shape(W, b, H, Wc, k4_groups<W>(chunk), chunk);
     return (int64_t)carve_batch<T>(nullptr, W, M, b, sh, H, Wc, upd).bytes;
 }
 

@@ -148,3 +148,12 @@ def test_batched_large_batch_multi_round_gather(gpu):
     e = batched_case(16, 1, (25, 25), 625, "fp64", step=3.0, sweeps=2)
     report("batched W16 b625 fp64", [e])
     assert e[0] < FP64_TOL and e[1] < FP64_TOL
+
+
+def test_batched_memory_budget_chunks_automatically(gpu, monkeypatch):
+    """A batch larger than the scratch budget (PTY_BATCH_BUDGET_MB) runs in
+    chunks chosen by the library -- same result as the oracle."""
+    monkeypatch.setenv("PTY_BATCH_BUDGET_MB", "1")          # 256 KB per position at W=64, M=2 -> chunks of 4
+    e = batched_case(64, 2, (4, 4), 16, "fp64", step=12.0)
+    report("batched W64 b16 budget-chunked", [e])
+    assert e[0] < FP64_TOL and e[1] < FP64_TOL
