@@ -527,7 +527,7 @@ def batched_leg(args, rank, world):
     hbm, _ = peaks()
     value = n / (per / 1e3)
     return {"workload": "config 5: batched semi-parallel rPIE, 80x80 scan (6400 positions), 256x256x3 modes, "
-                        f"batch {b} split over {world} GPU(s), NCCL all-reduce of the update terms per batch",
+                        f"batch {b} split spatially over {world} GPU(s): halo rows to their owner + all-gather of owned rows, probe terms all-reduced (partition.py)",
             "value": value, "unit": "positions/s", "ms_per_iteration": per, "iterations_per_s": 1e3 / per,
             "scaling": "strong", "roofline_frac": value * B_POS / (hbm * 1e9 * world),
             "error_trace_last": st.error_trace[-1]}

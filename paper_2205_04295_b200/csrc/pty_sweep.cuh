@@ -224,11 +224,19 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
                 my_target += (unsigned)P.cps;
                 if (threadIdx.x == 0) {
                     unsigned int one = 1u, seen;
+#ifdef PTY_BAR_RED
+                    // arrival without a returned value: polling starts without
+                    // waiting for the atomic's round trip
+                    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(my_bar), "r"(one) : "memory");
+#else
                     asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(seen) : "l"(my_bar), "r"(one) : "memory");
+#endif
                     while (true) {
                         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(my_bar) : "memory");
                         if ((int)(seen - my_target) >= 0) break;
+#ifndef PTY_BAR_SPIN
                         __nanosleep(20);
+#endif
                     }
                 }
                 __syncthreads();
