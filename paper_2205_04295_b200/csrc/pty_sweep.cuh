@@ -29,6 +29,7 @@ constexpr int kSweepThreads = 256;
 #endif
 constexpr int kSweepMaxCtasPerSm = 2;
 constexpr int kMaxSlots = 24;
+constexpr int kStagedRows = 16;        // rows per staged P1/P4 task (one 128-byte scratch line per column)
 constexpr int kMaxModes = 8;
 
 struct SlotDev {
@@ -55,6 +56,7 @@ struct SweepDev {
     int cps;                      // CTAs per slot (slot_local)
     unsigned int* slot_bar;       // [nslots][32] per-slot barrier counters (slot_local)
     int pair;                     // > 0: slots s and s + spp share the same SMs (virtual CTA index below)
+    int pair_offset;              // > 0: slot s + spp starts after slot s finished this many phases
     unsigned int* sm_pair;        // [8 + 256]: SM-id bitmap, CTAs per SM (zeroed per launch)
     // workspace
     unsigned int* barrier;
@@ -185,7 +187,13 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
     int vcta = cta;                                        // task-enumeration index (SM-paired in slot-local mode)
     const int ncta = CL ? (int)cluster_size() : (int)gridDim.x;
     const size_t WW = (size_t)W * W;
-    const int nq = W / 4;
+    // staged row tasks: blocks of RTS rows owned by a team of RTS groups
+    constexpr int RTS = kStagedRows, TEAM_S = RTS * B, NTEAM_S = kSweepThreads / TEAM_S;
+    constexpr int LSS = block_line_stride<W, RTS>();
+    static_assert(kSweepThreads % TEAM_S == 0, "a staged team must divide the CTA");
+    const int team_s = tid / TEAM_S, tl_s = tid % TEAM_S, gi_s = tl_s / B;
+    const int rows_per_task = P.p4_staged ? RTS : 4;           // row tasks: blocks (staged) or quads
+    const int nq = W / rows_per_task;
     const int team = tid / TEAM, tl = tid % TEAM, gi = tl / B, b = tid % B, grp = tid / B;
     const unsigned gmask = group_mask<W>();
     const UpdateParams U{P.alpha_o, P.alpha_p, P.beta, P.gamma, P.eps_rel, P.update_probe};
@@ -270,8 +278,8 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
         const C* probes = reinterpret_cast<const C*>(P.slot[s].probes);
         T* ppg = reinterpret_cast<T*>(P.ppg) + (size_t)s * WW;
         T pk = T(0);
-        for (int i = tid; i < 4 * W; i += NT) {
-            const size_t off = (size_t)(4 * rq) * W + i;
+        for (int i = tid; i < rows_per_task * W; i += NT) {
+            const size_t off = (size_t)(rows_per_task * rq) * W + i;
             T pp = T(0);
             for (int m = 0; m < M; ++m) pp += norm2(probes[m * WW + off]);
             ppg[off] = pp;
@@ -310,6 +318,21 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
             if (my_slot >= S) return;                          // idle CTA: no task in any phase
             local = true;
             my_bar = P.slot_bar + 32 * my_slot;
+            // anti-phase start (PTY_SLOT_PAIR=2): the second slot on an SM set
+            // begins once its partner slot has finished P1 and P2 of step 0, so
+            // the two CTAs of an SM run different phases instead of the same
+            const int spp = P.pair / P.cps;
+            if (P.pair > 0 && P.pair_offset > 0 && my_slot >= spp && tid == 0) {
+                const unsigned int* pb = P.slot_bar + 32 * (my_slot - spp);
+                const unsigned int want = (unsigned)(P.pair_offset * P.cps);
+                while (true) {
+                    unsigned int seen;
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(pb) : "memory");
+                    if (seen >= want) break;
+                    __nanosleep(100);
+                }
+            }
+            __syncthreads();
         }
     }
 
@@ -320,6 +343,9 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
         }
     };
     for (int step = 0; step < N; ++step) {
+#ifdef PTY_PROBE
+        if (blockIdx.x == 0 && tid == 0) pty_probe_step = step;
+#endif
         stamp(step, 0);
         if (tid < S) {   // status only changes in P4 / phase 0, both behind a barrier
             const int s = s0 + tid;
@@ -340,23 +366,23 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
         }
         __syncthreads();
         // ---------------------------------------------------------- P1 rows
-        if (P.p4_staged && P.p1_staged) {
-            C* lines_m = reinterpret_cast<C*>(region) + (size_t)team * M * 4 * LS4;
-            T* red4_s = reinterpret_cast<T*>(reinterpret_cast<C*>(region) + (size_t)NTEAM * M * 4 * LS4) + team * 4;
-            for (int task = vcta * NTEAM + team; task < S * nq; task += ncta * NTEAM) {
+        if (P.p4_staged) {
+            C* lines_m = reinterpret_cast<C*>(region) + (size_t)team_s * M * RTS * LSS;
+            T* red_s = reinterpret_cast<T*>(reinterpret_cast<C*>(region) + (size_t)NTEAM_S * M * RTS * LSS) + team_s * RTS;
+            for (int task = vcta * NTEAM_S + team_s; task < S * nq; task += ncta * NTEAM_S) {
                 const int s = s0 + task / nq, rq = task % nq;
                 if (s_dead[s]) continue;
                 const SlotDev& sl = P.slot[s];
                 const int j = s_j[s];
                 const char* It = reinterpret_cast<const char*>(reinterpret_cast<const T*>(sl.patterns_t) + (size_t)j * WW +
-                                                               (size_t)4 * rq * W);
-                for (int q = tl; q < (int)(4 * W * sizeof(T) / 128); q += TEAM)
+                                                               (size_t)RTS * rq * W);
+                for (int q = tl_s; q < (int)(RTS * W * sizeof(T) / 128); q += TEAM_S)
                     asm volatile("prefetch.global.L2 [%0];" ::"l"(It + q * 128));
                 C* stg = P.sense == PTY_SENSE_XCORR_A ? reinterpret_cast<C*>(sl.stage) + (size_t)j * 2 * WW : nullptr;
                 T om;
-#define PTY_P1S(MM) om = task_row_fwd_staged<T, W, MM>(tw, lines_m, red4_s, team, tl, gi, b, gmask, \
+#define PTY_P1S(MM) om = task_rows_fwd_block<T, W, MM, RTS>(tw, lines_m, red_s, team_s, tl_s, gi_s, b, gmask, \
                     reinterpret_cast<const C*>(sl.obj), sl.Wc, s_ar[s], s_ac[s], reinterpret_cast<const C*>(sl.probes), rq, \
-                    scratch + (size_t)s * M * WW, stg, &s_mbar[grp], &mphase)
+                    scratch + (size_t)s * M * WW, stg)
                 switch (M) {
                     case 1: PTY_P1S(1); break;
                     case 2: PTY_P1S(2); break;
@@ -364,7 +390,7 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
                     default: PTY_P1S(4); break;
                 }
 #undef PTY_P1S
-                if (tl == 0) omax_part[(size_t)s * nq + rq] = om;
+                if (tl_s == 0) omax_part[(size_t)s * nq + rq] = om;
             }
         } else
         for (int task = vcta * NTEAM + team; task < S * M * nq; task += ncta * NTEAM) {
@@ -421,6 +447,46 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
         phase_sync();
         stamp(step, 6);
         // --------------------------------------- P4 rows (inverse) + update
+        if (P.p4_staged) {
+            C* lines_m = reinterpret_cast<C*>(region) + (size_t)team_s * M * RTS * LSS;
+            T* red_s = reinterpret_cast<T*>(reinterpret_cast<C*>(region) + (size_t)NTEAM_S * M * RTS * LSS) + team_s * RTS;
+            for (int task = vcta * NTEAM_S + team_s; task < S * nq; task += ncta * NTEAM_S) {
+                const int s = s0 + task / nq, rq = task % nq;
+                if (s_dead[s]) continue;
+                const SlotDev& sl = P.slot[s];
+                const int j = s_j[s];
+                const T* pkp = peak_part + ((size_t)(step & 1) * P.nslots + s) * nq;
+                const T* omp = omax_part + (size_t)s * nq;
+                T peak = T(0), omax = T(0);
+                for (int q = b; q < nq; q += B) {
+                    peak = fmax(peak, pkp[q]);
+                    omax = fmax(omax, omp[q]);
+                }
+                peak = group_max<B>(peak);
+                omax = group_max<B>(omax);
+                if (peak == T(0)) {                            // engine.py:132-134
+                    if (tl_s == 0) atomicOr(sl.status, PTY_ERR_PROBE_ZERO);
+                    continue;
+                }
+                if (P.update_probe && omax == T(0)) {          // engine.py:145-147
+                    if (tl_s == 0) atomicOr(sl.status, PTY_ERR_OBJECT_ZERO);
+                    continue;
+                }
+                C* stg = P.sense == PTY_SENSE_XCORR_A ? reinterpret_cast<C*>(sl.stage) + (size_t)j * 2 * WW : nullptr;
+                T npk;
+#define PTY_P4S(MM) npk = task_rows_inv_block<T, W, MM, RTS>(tw, lines_m, red_s, team_s, tl_s, gi_s, b, gmask, \
+                    scratch + (size_t)s * M * WW, rq, reinterpret_cast<C*>(sl.obj), reinterpret_cast<T*>(P.ppg) + (size_t)s * WW, \
+                    sl.Wc, s_ar[s], s_ac[s], reinterpret_cast<C*>(sl.probes), peak, omax, U, stg)
+                switch (M) {
+                    case 1: PTY_P4S(1); break;
+                    case 2: PTY_P4S(2); break;
+                    case 3: PTY_P4S(3); break;
+                    default: PTY_P4S(4); break;   // host enables staging only for M <= 4
+                }
+#undef PTY_P4S
+                if (tl_s == 0) peak_part[((size_t)((step + 1) & 1) * P.nslots + s) * nq + rq] = npk;
+            }
+        } else
         for (int task = vcta * NTEAM + team; task < S * nq; task += ncta * NTEAM) {
             const int s = s0 + task / nq, rq = task % nq;
             if (s_dead[s]) continue;
@@ -445,32 +511,21 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
                 continue;
             }
             C* stg = P.sense == PTY_SENSE_XCORR_A ? reinterpret_cast<C*>(sl.stage) + (size_t)j * 2 * WW : nullptr;
-            T npk;
-            if (P.p4_staged) {
-                C* lines_m = reinterpret_cast<C*>(region) + (size_t)team * M * 4 * LS4;
-                T* red4_s = reinterpret_cast<T*>(reinterpret_cast<C*>(region) + (size_t)NTEAM * M * 4 * LS4) + team * 4;
-#define PTY_P4S(MM) npk = task_row_inv_update_staged<T, W, MM>(tw, lines_m, red4_s, team, tl, gi, b, gmask, \
-                    scratch + (size_t)s * M * WW, rq, reinterpret_cast<C*>(sl.obj), reinterpret_cast<T*>(P.ppg) + (size_t)s * WW, \
-                    sl.Wc, s_ar[s], s_ac[s], reinterpret_cast<C*>(sl.probes), peak, omax, U, stg)
-                switch (M) {
-                    case 1: PTY_P4S(1); break;
-                    case 2: PTY_P4S(2); break;
-                    case 3: PTY_P4S(3); break;
-                    default: PTY_P4S(4); break;   // host enables staging only for M <= 4
-                }
-#undef PTY_P4S
-            } else {
-                npk = task_row_inv_update<T, W>(tw, lines, numer, ppacc, nppacc, red4_p4, team, tl, gi, b, gmask,
-                                                scratch + (size_t)s * M * WW, M, rq, reinterpret_cast<C*>(sl.obj),
-                                                reinterpret_cast<T*>(P.ppg) + (size_t)s * WW,
-                                                sl.Wc, s_ar[s], s_ac[s], reinterpret_cast<C*>(sl.probes), peak,
-                                                omax, U, stg);
-            }
+            const T npk = task_row_inv_update<T, W>(tw, lines, numer, ppacc, nppacc, red4_p4, team, tl, gi, b, gmask,
+                                                    scratch + (size_t)s * M * WW, M, rq, reinterpret_cast<C*>(sl.obj),
+                                                    reinterpret_cast<T*>(P.ppg) + (size_t)s * WW,
+                                                    sl.Wc, s_ar[s], s_ac[s], reinterpret_cast<C*>(sl.probes), peak,
+                                                    omax, U, stg);
             if (tl == 0) peak_part[((size_t)((step + 1) & 1) * P.nslots + s) * nq + rq] = npk;
         }
         stamp(step, 7);
         phase_sync();
         stamp(step, 8);
+        if (P.timeline && step == 0 && tid == 0) {      // debug: the CTA's SM id replaces stamp (0, 8)
+            unsigned sm;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            P.timeline[(size_t)8 * gridDim.x + blockIdx.x] = sm;
+        }
     }
 }
 

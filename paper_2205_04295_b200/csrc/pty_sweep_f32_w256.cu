@@ -3,3 +3,10 @@
 namespace pty {
 template int run_sweep<float, 256>(const PtySweepArgs*, cudaStream_t);
 }
+
+#ifdef PTY_PROBE
+// debug: the probe stamps of the last sweep (64 steps x 32 slots)
+extern "C" __attribute__((visibility("default"))) int pty_probe_read(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, pty::pty_probe_buf, sizeof(pty::pty_probe_buf)) == cudaSuccess ? 0 : 1;
+}
+#endif

@@ -125,12 +125,14 @@ int run_sweep_lines(const PtySweepArgs* a, cudaStream_t st) {
     P.resident = (want_res && res_fit && (long)S * W <= (long)grid_ctas * NGRP && env_int("PTY_CLUSTER", 0) == 0) ? 1 : 0;
     // P4 staged: M*4 padded lines per team (M <= 4)
     constexpr int NTEAM4 = kSweepThreads / (4 * Shape<W>::B);
-    const size_t p4s_bytes = (size_t)NTEAM4 * M * 4 * team_line_stride<W>() * sizeof(cplx<T>) + NTEAM4 * 4 * sizeof(T);
+    constexpr int RTS = kStagedRows, NTEAM_S = kSweepThreads / (RTS * Shape<W>::B);
+    const size_t p4s_bytes = (size_t)NTEAM_S * M * RTS * block_line_stride<W, RTS>() * sizeof(cplx<T>) +
+                             (size_t)NTEAM_S * RTS * sizeof(T);
     size_t phase = P.resident ? res_phase : base_phase;
     const bool p4s_fit = 2 * (sweep_smem_fixed<T, W>() + std::max(phase, p4s_bytes) + 1024) <= max_smem_per_sm();
     P.p4_staged = (env_int("PTY_P4_STAGED", 1) && M <= 4 && p4s_fit) ? 1 : 0;
     if (P.p4_staged) phase = std::max(phase, p4s_bytes);
-    P.p1_staged = P.p4_staged && env_int("PTY_P1_STAGED", 1);
+    P.p1_staged = P.p4_staged;                 // staged P1 and P4 share the row-block task layout
     const size_t smem = sweep_smem_fixed<T, W>() + phase;
     if (smem > max_dyn_smem()) return PTY_ERR_ARGUMENT;
     int K = std::max(0, env_int("PTY_CLUSTER", 0));
@@ -175,15 +177,17 @@ int run_sweep_lines(const PtySweepArgs* a, cudaStream_t st) {
         if ((long)S * W > (long)grid * NGRP) P.resident = 0;   // more than one column task per group
         // slot-local barriers: one round of tasks in every phase and the same
         // CTA range per slot for row-quad tasks (teams) and column tasks (groups)
-        const int cps_rows = (W / 4) / NTEAM4, cps_cols = W / NGRP;
+        const int cps_rows = P.p4_staged ? (W / RTS) / NTEAM_S : (W / 4) / NTEAM4, cps_cols = W / NGRP;
+        const bool rows_even = P.p4_staged ? (W / RTS) % NTEAM_S == 0 : (W / 4) % NTEAM4 == 0;
         P.cps = cps_rows;
         P.slot_local = (env_int("PTY_SLOT_BARRIER", 1) && P.p1_staged && P.p4_staged && P.resident &&
                         cps_rows == cps_cols && cps_rows >= 1 && (long)S * cps_rows <= grid &&
-                        (W / 4) % NTEAM4 == 0 && W % NGRP == 0) ? 1 : 0;
+                        rows_even && W % NGRP == 0) ? 1 : 0;
         P.slot_bar = L.slot_bar;
         // two slots per SM set when the slots outnumber one CTA per SM
         const int spp = (grid / 2) / std::max(1, cps_rows);
-        P.pair = (P.slot_local && per_sm == 2 && S > spp && S <= 2 * spp && env_int("PTY_SLOT_PAIR", 0)) ? spp * cps_rows : 0;
+        P.pair = (P.slot_local && per_sm == 2 && S > spp && S <= 2 * spp && env_int("PTY_SLOT_PAIR", 1)) ? spp * cps_rows : 0;
+        P.pair_offset = P.pair > 0 ? std::max(0, env_int("PTY_PAIR_OFFSET", 2)) : 0;
         P.sm_pair = L.sm_pair;
     }
 

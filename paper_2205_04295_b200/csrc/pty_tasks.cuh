@@ -14,6 +14,24 @@
 
 namespace pty {
 
+#ifdef PTY_PROBE
+// debug build (-DPTY_PROBE): globaltimer stamps of CTA 0 / thread 0 inside
+// the P1 and P4 task bodies, per step ([step][32]); read back with
+// cudaMemcpyFromSymbol by the host (pty_probe_read)
+__device__ unsigned long long pty_probe_buf[64][32];
+__device__ int pty_probe_step;
+__device__ __forceinline__ void probe_stamp(int k) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && pty_probe_step < 64) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        pty_probe_buf[pty_probe_step][k] = t;
+    }
+}
+#define PTY_PROBE_STAMP(k) probe_stamp(k)
+#else
+#define PTY_PROBE_STAMP(k)
+#endif
+
 template <int TEAM>
 __device__ __forceinline__ void team_sync(int team) {
     if constexpr (TEAM <= 32) {
@@ -67,6 +85,28 @@ template <int W> __device__ __forceinline__ int slot_col(int b, int q) {
         return (b >> 2) + 8 * (2 * (b & 3) + (q >> 2)) + 64 * (q & 3);
     else
         return b + B * (q / B) + A * (q % B);
+}
+
+// Line stride of the staged lines of an RT-row block: >= W + W/B + 1 (the
+// padded line plus the exchange) and = 1 (mod 16) for RT = 16 (the 16 rows of
+// one column land in 16 different 8-byte bank pairs: conflict-free transposes),
+// = 4 (mod 16) for RT = 4 (team_line_stride).
+template <int W, int RT> __host__ __device__ constexpr int block_line_stride() {
+    return RT == 4 ? team_line_stride<W>() : ((W + W / Shape<W>::B + 1 + 14) / 16) * 16 + 1;
+}
+
+// Team-level max of one value per group over RT groups; red = RT shared slots of the team.
+template <int W, int RT, typename T>
+__device__ __forceinline__ T team_maxn(T v, T* red, int team, int gi, int b) {
+    constexpr int B = Shape<W>::B, TEAM = RT * B;
+    v = group_max<B>(v);
+    if (b == 0) red[gi] = v;
+    team_sync<TEAM>(team);
+    T r = red[0];
+#pragma unroll
+    for (int g = 1; g < RT; ++g) r = fmax(r, red[g]);
+    team_sync<TEAM>(team);
+    return r;
 }
 
 // Team-level max of one value per group (4 groups); red4 = 4 shared slots of the team.
@@ -129,54 +169,33 @@ __device__ __forceinline__ T task_row_fwd(const cplx<T>* tw, cplx<T>* xch, cplx<
     return res;
 }
 
-// Row pass, staged variant: team task (row quad rq, ALL modes) of one
-// position.  Every mode's probe row is brought into the group's mode lines by
-// bulk copies (one elected lane, the group's mbarrier) while the object row is
-// loaded into registers, so all of the task's inputs are in flight at once;
-// each line is then overwritten in place by its exit wave
-// (lines[(m*4 + gi)*LS4 + pad(n)]), transformed, and written transposed
-// ([m][kc][r]) straight from the lines.  Same arithmetic as task_row_fwd.
-// Returns the team's max|o|^2.
-template <typename T, int W, int MODES>
-__device__ __forceinline__ T task_row_fwd_staged(const cplx<T>* tw, cplx<T>* lines, T* red4, int team, int tl, int gi,
+// Row pass, staged: team task (block blk of RT consecutive rows, ALL modes)
+// of one position.  A team is RT line groups; group gi owns row r = RT*blk +
+// gi.  The object row is loaded once into registers, every mode's probe row is
+// loaded and its exit wave C * P_m * o_j staged in the team's lines
+// (lines[(m*RT + gi)*LS + pad(n)]); every line is transformed in place and the
+// block is written transposed ([m][kc][r]) straight from the lines.  With RT =
+// 16 one column of the block is 16 consecutive rows = one 128-byte line of
+// scratch, so the transposed stores are full-line writes (with RT = 4 they
+// were 32-byte pieces of four lines -- the P1 store time measured 2.6 of 7.5
+// us per task).  Same arithmetic as task_row_fwd.  Returns the team's max|o|^2.
+template <typename T, int W, int MODES, int RT>
+__device__ __forceinline__ T task_rows_fwd_block(const cplx<T>* tw, cplx<T>* lines, T* red, int team, int tl, int gi,
                                                  int b, unsigned gmask, const cplx<T>* obj, int Wc, int ar, int ac,
-                                                 const cplx<T>* probes, int rq, cplx<T>* dst_pos, cplx<T>* stg_o,
-                                                 unsigned long long* mbar, unsigned* mphase) {
+                                                 const cplx<T>* probes, int blk, cplx<T>* dst_pos, cplx<T>* stg_o) {
     using C = cplx<T>;
-    constexpr int A = Shape<W>::A, B = Shape<W>::B, TEAM = 4 * B, LS4 = team_line_stride<W>();
+    constexpr int A = Shape<W>::A, B = Shape<W>::B, TEAM = RT * B, LS = block_line_stride<W, RT>();
     const size_t WW = (size_t)W * W;
-    const int r = 4 * rq + gi;
+    const int r = RT * blk + gi;
     const C* orow = obj + (size_t)(ar + r) * Wc + ac;
     const C* prow = probes + (size_t)r * W;
-#ifdef PTY_TMA_LINES
-    if (b == 0) {
-        fence_proxy_async();
-        mbar_expect_tx(mbar, (unsigned)(MODES * W * sizeof(C)));
-#pragma unroll
-        for (int m = 0; m < MODES; ++m)
-            bulk_g2s(lines + (m * 4 + gi) * LS4, prow + m * WW, (unsigned)(W * sizeof(C)), mbar);
-    }
-    C ov[A], pv[A];
-#pragma unroll
-    for (int a = 0; a < A; ++a) ov[a] = orow[B * a + b];
-#else
-#ifdef PTY_P1_CPASYNC
-    // modes >= 1: probe rows straight into their (still unpadded) lines
-#pragma unroll
-    for (int m = 1; m < MODES; ++m)
-#pragma unroll
-        for (int i = 0; i < W / (2 * B); ++i) {
-            const int q = b + B * i;
-            cp_async<16>(lines + (m * 4 + gi) * LS4 + 2 * q, prow + m * WW + 2 * q);
-        }
-#endif
+    PTY_PROBE_STAMP(0);
     C ov[A], pv[A];
 #pragma unroll
     for (int a = 0; a < A; ++a) {
         ov[a] = orow[B * a + b];
         pv[a] = prow[B * a + b];
     }
-#endif
     T om = T(0);
 #pragma unroll
     for (int a = 0; a < A; ++a) om = fmax(om, norm2(ov[a]));
@@ -185,69 +204,40 @@ __device__ __forceinline__ T task_row_fwd_staged(const cplx<T>* tw, cplx<T>* lin
 #pragma unroll
         for (int a = 0; a < A; ++a) stg[B * a + b] = ov[a];
     }
-#ifdef PTY_TMA_LINES
-    mbar_wait(mbar, *mphase);
-    *mphase ^= 1u;
-#pragma unroll
-    for (int m = 0; m < MODES; ++m) {
-        C* line = lines + (m * 4 + gi) * LS4;
-#pragma unroll
-        for (int a = 0; a < A; ++a) pv[a] = line[B * a + b];          // P_m row, contiguous
-        __syncwarp(gmask);
-#pragma unroll
-        for (int a = 0; a < A; ++a) {
-            const int n = B * a + b;
-            line[pad<W>(n)] = scale(pv[a] * ov[a], checker<T>(r, n));
-        }
-    }
-#elif defined(PTY_P1_CPASYNC)
-    cp_async_wait_all();
-    __syncwarp(gmask);
-#pragma unroll
-    for (int m = 0; m < MODES; ++m) {
-        C* line = lines + (m * 4 + gi) * LS4;
-        if (m > 0) {
-#pragma unroll
-            for (int a = 0; a < A; ++a) pv[a] = line[B * a + b];
-            __syncwarp(gmask);
-        }
-#pragma unroll
-        for (int a = 0; a < A; ++a) {
-            const int n = B * a + b;
-            line[pad<W>(n)] = scale(pv[a] * ov[a], checker<T>(r, n));
-        }
-    }
-#else
-    team_sync<TEAM>(team);                                    // lines free
+    PTY_PROBE_STAMP(1);
+    PTY_PROBE_STAMP(2);
 #pragma unroll
     for (int m = 0; m < MODES; ++m) {
         if (m > 0) {
 #pragma unroll
             for (int a = 0; a < A; ++a) pv[a] = prow[m * WW + B * a + b];
         }
-        C* line = lines + (m * 4 + gi) * LS4;
+        C* line = lines + (m * RT + gi) * LS;
 #pragma unroll
         for (int a = 0; a < A; ++a) {
             const int n = B * a + b;
             line[pad<W>(n)] = scale(pv[a] * ov[a], checker<T>(r, n));
         }
     }
-#endif
     __syncwarp(gmask);
+    PTY_PROBE_STAMP(3);
 #pragma unroll 1
-    for (int m = 0; m < MODES; ++m) line_fft<T, W, false>(lines + (m * 4 + gi) * LS4, tw, b, gmask);
+    for (int m = 0; m < MODES; ++m) line_fft<T, W, false>(lines + (m * RT + gi) * LS, tw, b, gmask);
+    PTY_PROBE_STAMP(4);
     team_sync<TEAM>(team);
+    PTY_PROBE_STAMP(5);
 #pragma unroll
     for (int m = 0; m < MODES; ++m) {
-        C* dst = dst_pos + m * WW + 4 * rq;
-        const C* lm = lines + m * 4 * LS4;
+        C* dst = dst_pos + m * WW + RT * blk;
+        const C* lm = lines + m * RT * LS;
 #pragma unroll
-        for (int i = 0; i < 4 * W / TEAM; ++i) {
+        for (int i = 0; i < RT * W / TEAM; ++i) {
             const int e = tl + i * TEAM;
-            dst[(size_t)(e >> 2) * W + (e & 3)] = lm[(e & 3) * LS4 + pad<W>(e >> 2)];
+            dst[(size_t)(e / RT) * W + (e % RT)] = lm[(e % RT) * LS + pad<W>(e / RT)];
         }
     }
-    return team_max4<W>(om, red4, team, gi, b);
+    PTY_PROBE_STAMP(6);
+    return team_maxn<W, RT>(om, red, team, gi, b);
 }
 
 // Column pass, group task (column kc) of one position: forward column DFTs of
@@ -572,31 +562,14 @@ __device__ __forceinline__ T task_row_inv_update(const cplx<T>* tw, cplx<T>* lin
 // gathered first and its accumulators in registers.  Same expressions and
 // mode order as task_row_inv_update (engine.py:119-150, 218-224,
 // fields.py:101-107).  Returns the team max of the next visit's sum_m |P_m|^2.
-// Every mode's 4 scratch rows of row quad rq straight into the team's lines
-// (LDGSTS: all 4 * W * MODES elements in flight at once, no register staging);
-// the caller waits with cp_async_wait_all() + a team sync.
-template <typename T, int W, int MODES>
-__device__ __forceinline__ void stage_rows_async(cplx<T>* lines, const cplx<T>* pos, int rq, int tl) {
-    constexpr int B = Shape<W>::B, TEAM = 4 * B, LS4 = team_line_stride<W>(), NE = 4 * W / TEAM;
-    const size_t WW = (size_t)W * W;
-#pragma unroll
-    for (int m = 0; m < MODES; ++m)
-#pragma unroll
-        for (int i = 0; i < NE; ++i) {
-            const int e = tl + i * TEAM;
-            cp_async<(int)sizeof(cplx<T>)>(&lines[(m * 4 + (e & 3)) * LS4 + pad<W>(e >> 2)],
-                                           &pos[m * WW + (size_t)(e >> 2) * W + 4 * rq + (e & 3)]);
-        }
-}
-
-template <typename T, int W, int MODES>
-__device__ __forceinline__ T task_row_inv_update_staged(const cplx<T>* tw, cplx<T>* lines, T* red4, int team,
-                                                        int tl, int gi, int b, unsigned gmask, const cplx<T>* pos,
-                                                        int rq, cplx<T>* obj, T* ppg, int Wc, int ar, int ac,
-                                                        cplx<T>* probes, T peak, T omax, const UpdateParams& U,
-                                                        cplx<T>* stg) {
+template <typename T, int W, int MODES, int RT>
+__device__ __forceinline__ T task_rows_inv_block(const cplx<T>* tw, cplx<T>* lines, T* red, int team,
+                                                 int tl, int gi, int b, unsigned gmask, const cplx<T>* pos,
+                                                 int blk, cplx<T>* obj, T* ppg, int Wc, int ar, int ac,
+                                                 cplx<T>* probes, T peak, T omax, const UpdateParams& U,
+                                                 cplx<T>* stg) {
     using C = cplx<T>;
-    constexpr int B = Shape<W>::B, TEAM = 4 * B, LS4 = team_line_stride<W>(), NE = 4 * W / TEAM;
+    constexpr int B = Shape<W>::B, TEAM = RT * B, LS = block_line_stride<W, RT>(), NE = RT * W / TEAM;
 #ifdef PTY_P4_CH
     constexpr int CH = MODES <= 3 ? PTY_P4_CH : (MODES <= 6 ? 2 : 1);
 #else
@@ -606,14 +579,15 @@ __device__ __forceinline__ T task_row_inv_update_staged(const cplx<T>* tw, cplx<
     const T invW2 = T(1) / (T(W) * T(W));
     const T alpha_o = T(U.alpha_o), alpha_p = T(U.alpha_p), beta = T(U.beta), gamma = T(U.gamma),
             eps_rel = T(U.eps_rel);
-#ifndef PTY_P4_LDGSTS
-    // the scratch rows of mode m+1 are in flight before mode m is stored to
-    // shared memory (two modes of loads outstanding per thread)
+    PTY_PROBE_STAMP(10);
+    // the block's scratch rows ([m][kc][RT*blk + row]: RT consecutive complex
+    // values per column -- a 128-byte line for RT = 16) into the team's lines;
+    // mode m+1's loads are in flight while mode m is stored to shared memory
     C cur[NE], nxt[NE];
 #pragma unroll
     for (int i = 0; i < NE; ++i) {
         const int e = tl + i * TEAM;
-        cur[i] = pos[(size_t)(e >> 2) * W + 4 * rq + (e & 3)];
+        cur[i] = pos[(size_t)(e / RT) * W + RT * blk + (e % RT)];
     }
     team_sync<TEAM>(team);                                     // lines free
 #pragma unroll
@@ -622,13 +596,13 @@ __device__ __forceinline__ T task_row_inv_update_staged(const cplx<T>* tw, cplx<
 #pragma unroll
             for (int i = 0; i < NE; ++i) {
                 const int e = tl + i * TEAM;
-                nxt[i] = pos[(m + 1) * WW + (size_t)(e >> 2) * W + 4 * rq + (e & 3)];
+                nxt[i] = pos[(m + 1) * WW + (size_t)(e / RT) * W + RT * blk + (e % RT)];
             }
         }
 #pragma unroll
         for (int i = 0; i < NE; ++i) {
             const int e = tl + i * TEAM;
-            lines[(m * 4 + (e & 3)) * LS4 + pad<W>(e >> 2)] = cur[i];
+            lines[(m * RT + (e % RT)) * LS + pad<W>(e / RT)] = cur[i];
         }
         if (m + 1 < MODES) {
 #pragma unroll
@@ -636,14 +610,12 @@ __device__ __forceinline__ T task_row_inv_update_staged(const cplx<T>* tw, cplx<
         }
     }
     team_sync<TEAM>(team);
-#else
-    stage_rows_async<T, W, MODES>(lines, pos, rq, tl);
-    cp_async_wait_all();
-    team_sync<TEAM>(team);
-#endif
+    PTY_PROBE_STAMP(11);
 #pragma unroll 1
-    for (int m = 0; m < MODES; ++m) line_fft<T, W, true>(lines + (m * 4 + gi) * LS4, tw, b, gmask);
+    for (int m = 0; m < MODES; ++m) line_fft<T, W, true>(lines + (m * RT + gi) * LS, tw, b, gmask);
+    PTY_PROBE_STAMP(12);
     team_sync<TEAM>(team);
+    PTY_PROBE_STAMP(13);
     const T dmax_p = beta * omax + (T(1) - beta) * omax;
     const T dmax_o = gamma * peak + (T(1) - gamma) * peak;
     T pk = T(0);
@@ -652,14 +624,14 @@ __device__ __forceinline__ T task_row_inv_update_staged(const cplx<T>* tw, cplx<
         C ov[CH], pv[MODES][CH];
 #pragma unroll
         for (int k = 0; k < CH; ++k) {
-            const int e = tl + (h + k) * TEAM, rr = e / W, c = e % W, r = 4 * rq + rr;
+            const int e = tl + (h + k) * TEAM, rr = e / W, c = e % W, r = RT * blk + rr;
             ov[k] = obj[(size_t)(ar + r) * Wc + ac + c];
 #pragma unroll
             for (int m = 0; m < MODES; ++m) pv[m][k] = probes[m * WW + (size_t)r * W + c];
         }
 #pragma unroll
         for (int k = 0; k < CH; ++k) {
-            const int e = tl + (h + k) * TEAM, rr = e / W, c = e % W, r = 4 * rq + rr;
+            const int e = tl + (h + k) * TEAM, rr = e / W, c = e % W, r = RT * blk + rr;
             const C o = ov[k];
             T dp = beta * omax + (T(1) - beta) * norm2(o);
             dp = dp + eps_rel * dmax_p;
@@ -669,7 +641,7 @@ __device__ __forceinline__ T task_row_inv_update_staged(const cplx<T>* tw, cplx<
             T npp = T(0);
 #pragma unroll
             for (int m = 0; m < MODES; ++m) {
-                const C X = lines[(m * 4 + rr) * LS4 + pad<W>(c)];
+                const C X = lines[(m * RT + rr) * LS + pad<W>(c)];
                 const C d = scale(X, checker<T>(r, c) * invW2) - om.mul(pv[m][k]);
                 numer = numer + mulc(d, pv[m][k]);
                 if (U.update_probe) {
@@ -693,8 +665,9 @@ __device__ __forceinline__ T task_row_inv_update_staged(const cplx<T>* tw, cplx<
             pk = fmax(pk, U.update_probe ? npp : ppk);
         }
     }
+    PTY_PROBE_STAMP(14);
     pk = group_max<B>(pk);
-    return team_max4<W>(pk, red4, team, gi, b);
+    return team_maxn<W, RT>(pk, red, team, gi, b);
 }
 
 }  // namespace pty
