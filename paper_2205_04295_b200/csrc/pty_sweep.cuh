@@ -336,6 +336,12 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
         }
     }
 
+    bool early = false;                                    // P1's probe rows already in flight (PTY_P1_EARLY)
+    int4 v_next = make_int4(0, 0, 0, 0);
+    if (tid < S) {
+        v_next = P.steptab[(size_t)(s0 + tid) * N];
+        s_dead[s0 + tid] = *(volatile const int*)P.slot[s0 + tid].status;   // phase-0 bounds errors
+    }
     auto stamp = [&](int step, int k) {
         if (P.timeline && step < P.timeline_steps) {
             __syncthreads();
@@ -347,22 +353,18 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
         if (blockIdx.x == 0 && tid == 0) pty_probe_step = step;
 #endif
         stamp(step, 0);
-        if (tid < S) {   // status only changes in P4 / phase 0, both behind a barrier
+        if (tid < S) {
             const int s = s0 + tid;
-#ifndef PTY_NO_STEPTAB
-            const int4 v = P.steptab[(size_t)s * N + step];     // (j, ar, ac): one load, no dependent lookup
-            s_dead[s] = *(volatile const int*)P.slot[s].status;
+            // (j, ar, ac) of this step, loaded one step ahead (phase 0 wrote the table)
+            const int4 v = v_next;
+            if (step + 1 < N) v_next = P.steptab[(size_t)s * N + step + 1];
+            // status only changes in P4 / phase 0, both behind a barrier.  In
+            // slot-local mode a CTA tracks its own slot's P4 errors itself (all
+            // of a slot's CTAs reduce the same maxima), so no reload per step
+            if (!local) s_dead[s] = *(volatile const int*)P.slot[s].status;
             s_j[s] = v.x;
             s_ar[s] = v.y;
             s_ac[s] = v.z;
-#else
-            const SlotDev& sl = P.slot[s];
-            const int j = sl.order[step];
-            s_dead[s] = *(volatile const int*)sl.status;
-            s_j[s] = j;
-            s_ar[s] = P.anchors[2 * (s * N + j)];
-            s_ac[s] = P.anchors[2 * (s * N + j) + 1];
-#endif
         }
         __syncthreads();
         // ---------------------------------------------------------- P1 rows
@@ -382,7 +384,7 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
                 T om;
 #define PTY_P1S(MM) om = task_rows_fwd_block<T, W, MM, RTS>(tw, lines_m, red_s, team_s, tl_s, gi_s, b, gmask, \
                     reinterpret_cast<const C*>(sl.obj), sl.Wc, s_ar[s], s_ac[s], reinterpret_cast<const C*>(sl.probes), rq, \
-                    scratch + (size_t)s * M * WW, stg)
+                    scratch + (size_t)s * M * WW, stg, early)
                 switch (M) {
                     case 1: PTY_P1S(1); break;
                     case 2: PTY_P1S(2); break;
@@ -390,6 +392,7 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
                     default: PTY_P1S(4); break;
                 }
 #undef PTY_P1S
+                early = false;
                 if (tl_s == 0) omax_part[(size_t)s * nq + rq] = om;
             }
         } else
@@ -455,28 +458,17 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
                 if (s_dead[s]) continue;
                 const SlotDev& sl = P.slot[s];
                 const int j = s_j[s];
+                // the maxima partials are reduced inside the task, while the
+                // block's scratch rows are already in flight (engine.py:132-134,
+                // 145-147 checked there: a failing slot returns its error bit)
                 const T* pkp = peak_part + ((size_t)(step & 1) * P.nslots + s) * nq;
                 const T* omp = omax_part + (size_t)s * nq;
-                T peak = T(0), omax = T(0);
-                for (int q = b; q < nq; q += B) {
-                    peak = fmax(peak, pkp[q]);
-                    omax = fmax(omax, omp[q]);
-                }
-                peak = group_max<B>(peak);
-                omax = group_max<B>(omax);
-                if (peak == T(0)) {                            // engine.py:132-134
-                    if (tl_s == 0) atomicOr(sl.status, PTY_ERR_PROBE_ZERO);
-                    continue;
-                }
-                if (P.update_probe && omax == T(0)) {          // engine.py:145-147
-                    if (tl_s == 0) atomicOr(sl.status, PTY_ERR_OBJECT_ZERO);
-                    continue;
-                }
                 C* stg = P.sense == PTY_SENSE_XCORR_A ? reinterpret_cast<C*>(sl.stage) + (size_t)j * 2 * WW : nullptr;
                 T npk;
+                int bad = 0;
 #define PTY_P4S(MM) npk = task_rows_inv_block<T, W, MM, RTS>(tw, lines_m, red_s, team_s, tl_s, gi_s, b, gmask, \
                     scratch + (size_t)s * M * WW, rq, reinterpret_cast<C*>(sl.obj), reinterpret_cast<T*>(P.ppg) + (size_t)s * WW, \
-                    sl.Wc, s_ar[s], s_ac[s], reinterpret_cast<C*>(sl.probes), peak, omax, U, stg)
+                    sl.Wc, s_ar[s], s_ac[s], reinterpret_cast<C*>(sl.probes), pkp, omp, nq, U, stg, bad)
                 switch (M) {
                     case 1: PTY_P4S(1); break;
                     case 2: PTY_P4S(2); break;
@@ -484,7 +476,26 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
                     default: PTY_P4S(4); break;   // host enables staging only for M <= 4
                 }
 #undef PTY_P4S
+                if (bad) {
+                    if (tl_s == 0) atomicOr(sl.status, bad);
+                    if (local && tid == 0) s_dead[s] = 1;     // every CTA of the slot sees the same maxima
+                    continue;
+                }
                 if (tl_s == 0) peak_part[((size_t)((step + 1) & 1) * P.nslots + s) * nq + rq] = npk;
+#ifdef PTY_P1_EARLY
+                // the next visit's P1 task of this CTA is the same row block:
+                // its probe rows (just updated by this team, ordered by the
+                // team barrier in the reduction above) load during the barrier
+                if (local && step + 1 < N) {
+                    switch (M) {
+                        case 1: issue_probe_rows<T, W, 1, RTS>(lines_m, gi_s, b, reinterpret_cast<const C*>(sl.probes), rq); break;
+                        case 2: issue_probe_rows<T, W, 2, RTS>(lines_m, gi_s, b, reinterpret_cast<const C*>(sl.probes), rq); break;
+                        case 3: issue_probe_rows<T, W, 3, RTS>(lines_m, gi_s, b, reinterpret_cast<const C*>(sl.probes), rq); break;
+                        default: issue_probe_rows<T, W, 4, RTS>(lines_m, gi_s, b, reinterpret_cast<const C*>(sl.probes), rq); break;
+                    }
+                    early = true;
+                }
+#endif
             }
         } else
         for (int task = vcta * NTEAM + team; task < S * nq; task += ncta * NTEAM) {
@@ -502,12 +513,9 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
             }
             peak = group_max<B>(peak);
             omax = group_max<B>(omax);
-            if (peak == T(0)) {                                // engine.py:132-134
-                if (tl == 0) atomicOr(sl.status, PTY_ERR_PROBE_ZERO);
-                continue;
-            }
-            if (P.update_probe && omax == T(0)) {              // engine.py:145-147
-                if (tl == 0) atomicOr(sl.status, PTY_ERR_OBJECT_ZERO);
+            if (peak == T(0) || (P.update_probe && omax == T(0))) {   // engine.py:132-134, 145-147
+                if (tl == 0) atomicOr(sl.status, peak == T(0) ? PTY_ERR_PROBE_ZERO : PTY_ERR_OBJECT_ZERO);
+                if (local && tid == 0) s_dead[s] = 1;
                 continue;
             }
             C* stg = P.sense == PTY_SENSE_XCORR_A ? reinterpret_cast<C*>(sl.stage) + (size_t)j * 2 * WW : nullptr;
@@ -526,6 +534,8 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
             asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
             P.timeline[(size_t)8 * gridDim.x + blockIdx.x] = sm;
         }
+        if (P.timeline && step == 1 && tid == 0 && P.timeline_steps > 1)   // ... and the virtual CTA index stamp (1, 8)
+            P.timeline[(size_t)17 * gridDim.x + blockIdx.x] = (unsigned long long)vcta;
     }
 }
 

@@ -179,10 +179,29 @@ __device__ __forceinline__ T task_row_fwd(const cplx<T>* tw, cplx<T>* xch, cplx<
 // scratch, so the transposed stores are full-line writes (with RT = 4 they
 // were 32-byte pieces of four lines -- the P1 store time measured 2.6 of 7.5
 // us per task).  Same arithmetic as task_row_fwd.  Returns the team's max|o|^2.
+#if defined(PTY_P1_EARLY) && !defined(PTY_P1_ASYNC)
+#define PTY_P1_ASYNC
+#endif
+// The probe rows of block blk, every mode, into the team's lines by cp.async:
+// lane b of group gi copies exactly the elements it later multiplies by o_j
+// (n = B*a + b of line (m, gi)), so its own cp.async wait makes them visible.
+template <typename T, int W, int MODES, int RT>
+__device__ __forceinline__ void issue_probe_rows(cplx<T>* lines, int gi, int b, const cplx<T>* probes, int blk) {
+    constexpr int A = Shape<W>::A, B = Shape<W>::B, LS = block_line_stride<W, RT>();
+    const cplx<T>* prow = probes + (size_t)(RT * blk + gi) * W;
+#pragma unroll
+    for (int m = 0; m < MODES; ++m) {
+        cplx<T>* line = lines + (m * RT + gi) * LS;
+#pragma unroll
+        for (int a = 0; a < A; ++a) cp_async<sizeof(cplx<T>)>(line + pad<W>(B * a + b), prow + (size_t)m * W * W + B * a + b);
+    }
+}
+
 template <typename T, int W, int MODES, int RT>
 __device__ __forceinline__ T task_rows_fwd_block(const cplx<T>* tw, cplx<T>* lines, T* red, int team, int tl, int gi,
                                                  int b, unsigned gmask, const cplx<T>* obj, int Wc, int ar, int ac,
-                                                 const cplx<T>* probes, int blk, cplx<T>* dst_pos, cplx<T>* stg_o) {
+                                                 const cplx<T>* probes, int blk, cplx<T>* dst_pos, cplx<T>* stg_o,
+                                                 bool probes_issued = false) {
     using C = cplx<T>;
     constexpr int A = Shape<W>::A, B = Shape<W>::B, TEAM = RT * B, LS = block_line_stride<W, RT>();
     const size_t WW = (size_t)W * W;
@@ -190,12 +209,22 @@ __device__ __forceinline__ T task_rows_fwd_block(const cplx<T>* tw, cplx<T>* lin
     const C* orow = obj + (size_t)(ar + r) * Wc + ac;
     const C* prow = probes + (size_t)r * W;
     PTY_PROBE_STAMP(0);
+#ifdef PTY_P1_ASYNC
+    // every mode's probe row straight into the lines (cp.async, no registers):
+    // one L2 round trip for all modes -- or none here when the previous P4
+    // issued them before its barrier (PTY_P1_EARLY)
+    if (!probes_issued) issue_probe_rows<T, W, MODES, RT>(lines, gi, b, probes, blk);
+    C ov[A];
+#pragma unroll
+    for (int a = 0; a < A; ++a) ov[a] = orow[B * a + b];
+#else
     C ov[A], pv[A];
 #pragma unroll
     for (int a = 0; a < A; ++a) {
         ov[a] = orow[B * a + b];
         pv[a] = prow[B * a + b];
     }
+#endif
     T om = T(0);
 #pragma unroll
     for (int a = 0; a < A; ++a) om = fmax(om, norm2(ov[a]));
@@ -206,6 +235,18 @@ __device__ __forceinline__ T task_rows_fwd_block(const cplx<T>* tw, cplx<T>* lin
     }
     PTY_PROBE_STAMP(1);
     PTY_PROBE_STAMP(2);
+#ifdef PTY_P1_ASYNC
+    cp_async_wait_all();
+#pragma unroll
+    for (int m = 0; m < MODES; ++m) {
+        C* line = lines + (m * RT + gi) * LS;
+#pragma unroll
+        for (int a = 0; a < A; ++a) {
+            const int n = B * a + b;
+            line[pad<W>(n)] = scale(line[pad<W>(n)] * ov[a], checker<T>(r, n));
+        }
+    }
+#else
 #pragma unroll
     for (int m = 0; m < MODES; ++m) {
         if (m > 0) {
@@ -219,6 +260,7 @@ __device__ __forceinline__ T task_rows_fwd_block(const cplx<T>* tw, cplx<T>* lin
             line[pad<W>(n)] = scale(pv[a] * ov[a], checker<T>(r, n));
         }
     }
+#endif
     __syncwarp(gmask);
     PTY_PROBE_STAMP(3);
 #pragma unroll 1
@@ -554,6 +596,32 @@ __device__ __forceinline__ T task_row_inv_update(const cplx<T>* tw, cplx<T>* lin
     return team_max4<W>(pk, red4, team, gi, b);
 }
 
+// This visit's max sum_m |P_m|^2 and max |o_j|^2 from their per-block partials
+// (every group reduces all of them: the result is uniform over the team).
+// false (and the error bit in `bad`) if the update is degenerate
+// (engine.py:132-134, 145-147).
+template <typename T, int B>
+__device__ __forceinline__ bool block_maxima(const T* peak_part, const T* omax_part, int n, int b, int update_probe,
+                                             T& peak, T& omax, int& bad) {
+    peak = T(0);
+    omax = T(0);
+    for (int q = b; q < n; q += B) {
+        peak = fmax(peak, peak_part[q]);
+        omax = fmax(omax, omax_part[q]);
+    }
+    peak = group_max<B>(peak);
+    omax = group_max<B>(omax);
+    if (peak == T(0)) {
+        bad = PTY_ERR_PROBE_ZERO;
+        return false;
+    }
+    if (update_probe && omax == T(0)) {
+        bad = PTY_ERR_OBJECT_ZERO;
+        return false;
+    }
+    return true;
+}
+
 // Row pass 2, staged variant (shared memory for all modes): team task (row
 // quad rq) of one position.  (1) the 4 rows of every mode are loaded into the
 // team's lines (lines[(m*4 + gi)*LS4 + pad(c)]), (2) every line is
@@ -566,8 +634,8 @@ template <typename T, int W, int MODES, int RT>
 __device__ __forceinline__ T task_rows_inv_block(const cplx<T>* tw, cplx<T>* lines, T* red, int team,
                                                  int tl, int gi, int b, unsigned gmask, const cplx<T>* pos,
                                                  int blk, cplx<T>* obj, T* ppg, int Wc, int ar, int ac,
-                                                 cplx<T>* probes, T peak, T omax, const UpdateParams& U,
-                                                 cplx<T>* stg) {
+                                                 cplx<T>* probes, const T* peak_part, const T* omax_part, int nparts,
+                                                 const UpdateParams& U, cplx<T>* stg, int& bad) {
     using C = cplx<T>;
     constexpr int B = Shape<W>::B, TEAM = RT * B, LS = block_line_stride<W, RT>(), NE = RT * W / TEAM;
 #ifdef PTY_P4_CH
@@ -579,16 +647,38 @@ __device__ __forceinline__ T task_rows_inv_block(const cplx<T>* tw, cplx<T>* lin
     const T invW2 = T(1) / (T(W) * T(W));
     const T alpha_o = T(U.alpha_o), alpha_p = T(U.alpha_p), beta = T(U.beta), gamma = T(U.gamma),
             eps_rel = T(U.eps_rel);
+    T peak, omax;
     PTY_PROBE_STAMP(10);
     // the block's scratch rows ([m][kc][RT*blk + row]: RT consecutive complex
     // values per column -- a 128-byte line for RT = 16) into the team's lines;
     // mode m+1's loads are in flight while mode m is stored to shared memory
+#ifndef PTY_P4_REGS
+    // every mode's rows in flight at once (cp.async, no register staging;
+    // PTY_P4_REGS: the register-staged loads, mode m+1 in flight while mode m
+    // is stored -- measured 1.2 % slower)
+    team_sync<TEAM>(team);                                     // lines free
+#pragma unroll
+    for (int m = 0; m < MODES; ++m) {
+#pragma unroll
+        for (int i = 0; i < NE; ++i) {
+            const int e = tl + i * TEAM;
+            cp_async<sizeof(C)>(lines + (m * RT + (e % RT)) * LS + pad<W>(e / RT),
+                                pos + m * WW + (size_t)(e / RT) * W + RT * blk + (e % RT));
+        }
+    }
+    if (!block_maxima<T, B>(peak_part, omax_part, nparts, b, U.update_probe, peak, omax, bad)) {
+        cp_async_wait_all();
+        return T(0);
+    }
+    cp_async_wait_all();
+#else
     C cur[NE], nxt[NE];
 #pragma unroll
     for (int i = 0; i < NE; ++i) {
         const int e = tl + i * TEAM;
         cur[i] = pos[(size_t)(e / RT) * W + RT * blk + (e % RT)];
     }
+    if (!block_maxima<T, B>(peak_part, omax_part, nparts, b, U.update_probe, peak, omax, bad)) return T(0);
     team_sync<TEAM>(team);                                     // lines free
 #pragma unroll
     for (int m = 0; m < MODES; ++m) {
@@ -609,6 +699,7 @@ __device__ __forceinline__ T task_rows_inv_block(const cplx<T>* tw, cplx<T>* lin
             for (int i = 0; i < NE; ++i) cur[i] = nxt[i];
         }
     }
+#endif
     team_sync<TEAM>(team);
     PTY_PROBE_STAMP(11);
 #pragma unroll 1
