@@ -336,7 +336,6 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
         }
     }
 
-    bool early = false;                                    // P1's probe rows already in flight (PTY_P1_EARLY)
     int4 v_next = make_int4(0, 0, 0, 0);
     if (tid < S) {
         v_next = P.steptab[(size_t)(s0 + tid) * N];
@@ -384,7 +383,7 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
                 T om;
 #define PTY_P1S(MM) om = task_rows_fwd_block<T, W, MM, RTS>(tw, lines_m, red_s, team_s, tl_s, gi_s, b, gmask, \
                     reinterpret_cast<const C*>(sl.obj), sl.Wc, s_ar[s], s_ac[s], reinterpret_cast<const C*>(sl.probes), rq, \
-                    scratch + (size_t)s * M * WW, stg, early)
+                    scratch + (size_t)s * M * WW, stg)
                 switch (M) {
                     case 1: PTY_P1S(1); break;
                     case 2: PTY_P1S(2); break;
@@ -392,7 +391,6 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
                     default: PTY_P1S(4); break;
                 }
 #undef PTY_P1S
-                early = false;
                 if (tl_s == 0) omax_part[(size_t)s * nq + rq] = om;
             }
         } else
@@ -482,20 +480,6 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
                     continue;
                 }
                 if (tl_s == 0) peak_part[((size_t)((step + 1) & 1) * P.nslots + s) * nq + rq] = npk;
-#ifdef PTY_P1_EARLY
-                // the next visit's P1 task of this CTA is the same row block:
-                // its probe rows (just updated by this team, ordered by the
-                // team barrier in the reduction above) load during the barrier
-                if (local && step + 1 < N) {
-                    switch (M) {
-                        case 1: issue_probe_rows<T, W, 1, RTS>(lines_m, gi_s, b, reinterpret_cast<const C*>(sl.probes), rq); break;
-                        case 2: issue_probe_rows<T, W, 2, RTS>(lines_m, gi_s, b, reinterpret_cast<const C*>(sl.probes), rq); break;
-                        case 3: issue_probe_rows<T, W, 3, RTS>(lines_m, gi_s, b, reinterpret_cast<const C*>(sl.probes), rq); break;
-                        default: issue_probe_rows<T, W, 4, RTS>(lines_m, gi_s, b, reinterpret_cast<const C*>(sl.probes), rq); break;
-                    }
-                    early = true;
-                }
-#endif
             }
         } else
         for (int task = vcta * NTEAM + team; task < S * nq; task += ncta * NTEAM) {

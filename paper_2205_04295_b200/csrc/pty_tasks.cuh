@@ -179,29 +179,10 @@ __device__ __forceinline__ T task_row_fwd(const cplx<T>* tw, cplx<T>* xch, cplx<
 // scratch, so the transposed stores are full-line writes (with RT = 4 they
 // were 32-byte pieces of four lines -- the P1 store time measured 2.6 of 7.5
 // us per task).  Same arithmetic as task_row_fwd.  Returns the team's max|o|^2.
-#if defined(PTY_P1_EARLY) && !defined(PTY_P1_ASYNC)
-#define PTY_P1_ASYNC
-#endif
-// The probe rows of block blk, every mode, into the team's lines by cp.async:
-// lane b of group gi copies exactly the elements it later multiplies by o_j
-// (n = B*a + b of line (m, gi)), so its own cp.async wait makes them visible.
-template <typename T, int W, int MODES, int RT>
-__device__ __forceinline__ void issue_probe_rows(cplx<T>* lines, int gi, int b, const cplx<T>* probes, int blk) {
-    constexpr int A = Shape<W>::A, B = Shape<W>::B, LS = block_line_stride<W, RT>();
-    const cplx<T>* prow = probes + (size_t)(RT * blk + gi) * W;
-#pragma unroll
-    for (int m = 0; m < MODES; ++m) {
-        cplx<T>* line = lines + (m * RT + gi) * LS;
-#pragma unroll
-        for (int a = 0; a < A; ++a) cp_async<sizeof(cplx<T>)>(line + pad<W>(B * a + b), prow + (size_t)m * W * W + B * a + b);
-    }
-}
-
 template <typename T, int W, int MODES, int RT>
 __device__ __forceinline__ T task_rows_fwd_block(const cplx<T>* tw, cplx<T>* lines, T* red, int team, int tl, int gi,
                                                  int b, unsigned gmask, const cplx<T>* obj, int Wc, int ar, int ac,
-                                                 const cplx<T>* probes, int blk, cplx<T>* dst_pos, cplx<T>* stg_o,
-                                                 bool probes_issued = false) {
+                                                 const cplx<T>* probes, int blk, cplx<T>* dst_pos, cplx<T>* stg_o) {
     using C = cplx<T>;
     constexpr int A = Shape<W>::A, B = Shape<W>::B, TEAM = RT * B, LS = block_line_stride<W, RT>();
     const size_t WW = (size_t)W * W;
@@ -209,22 +190,12 @@ __device__ __forceinline__ T task_rows_fwd_block(const cplx<T>* tw, cplx<T>* lin
     const C* orow = obj + (size_t)(ar + r) * Wc + ac;
     const C* prow = probes + (size_t)r * W;
     PTY_PROBE_STAMP(0);
-#ifdef PTY_P1_ASYNC
-    // every mode's probe row straight into the lines (cp.async, no registers):
-    // one L2 round trip for all modes -- or none here when the previous P4
-    // issued them before its barrier (PTY_P1_EARLY)
-    if (!probes_issued) issue_probe_rows<T, W, MODES, RT>(lines, gi, b, probes, blk);
-    C ov[A];
-#pragma unroll
-    for (int a = 0; a < A; ++a) ov[a] = orow[B * a + b];
-#else
     C ov[A], pv[A];
 #pragma unroll
     for (int a = 0; a < A; ++a) {
         ov[a] = orow[B * a + b];
         pv[a] = prow[B * a + b];
     }
-#endif
     T om = T(0);
 #pragma unroll
     for (int a = 0; a < A; ++a) om = fmax(om, norm2(ov[a]));
@@ -235,18 +206,6 @@ __device__ __forceinline__ T task_rows_fwd_block(const cplx<T>* tw, cplx<T>* lin
     }
     PTY_PROBE_STAMP(1);
     PTY_PROBE_STAMP(2);
-#ifdef PTY_P1_ASYNC
-    cp_async_wait_all();
-#pragma unroll
-    for (int m = 0; m < MODES; ++m) {
-        C* line = lines + (m * RT + gi) * LS;
-#pragma unroll
-        for (int a = 0; a < A; ++a) {
-            const int n = B * a + b;
-            line[pad<W>(n)] = scale(line[pad<W>(n)] * ov[a], checker<T>(r, n));
-        }
-    }
-#else
 #pragma unroll
     for (int m = 0; m < MODES; ++m) {
         if (m > 0) {
@@ -260,7 +219,6 @@ __device__ __forceinline__ T task_rows_fwd_block(const cplx<T>* tw, cplx<T>* lin
             line[pad<W>(n)] = scale(pv[a] * ov[a], checker<T>(r, n));
         }
     }
-#endif
     __syncwarp(gmask);
     PTY_PROBE_STAMP(3);
 #pragma unroll 1
