@@ -171,14 +171,14 @@ __device__ __forceinline__ T task_row_fwd(const cplx<T>* tw, cplx<T>* xch, cplx<
 
 // Row pass, staged: team task (block blk of RT consecutive rows, ALL modes)
 // of one position.  A team is RT line groups; group gi owns row r = RT*blk +
-// gi.  The object row is loaded once into registers, every mode's probe row is
-// loaded and its exit wave C * P_m * o_j staged in the team's lines
-// (lines[(m*RT + gi)*LS + pad(n)]); every line is transformed in place and the
-// block is written transposed ([m][kc][r]) straight from the lines.  With RT =
-// 16 one column of the block is 16 consecutive rows = one 128-byte line of
-// scratch, so the transposed stores are full-line writes (with RT = 4 they
-// were 32-byte pieces of four lines -- the P1 store time measured 2.6 of 7.5
-// us per task).  Same arithmetic as task_row_fwd.  Returns the team's max|o|^2.
+// gi.  The object row is loaded once into registers; every mode's exit wave
+// C * P_m * o_j enters the line transform from registers (no staging pass)
+// and the spectrum lands in the team's lines (lines[(m*RT + gi)*LS +
+// pad(k)]); the block is then written transposed ([m][kc][r]) from the lines.
+// With RT = 16 one column of the block is 16 consecutive rows = one 128-byte
+// line of scratch, so the transposed stores are full-line writes (with RT = 4
+// they were 32-byte pieces of four lines).  Same arithmetic as task_row_fwd.
+// Returns the team's max|o|^2.
 template <typename T, int W, int MODES, int RT>
 __device__ __forceinline__ T task_rows_fwd_block(const cplx<T>* tw, cplx<T>* lines, T* red, int team, int tl, int gi,
                                                  int b, unsigned gmask, const cplx<T>* obj, int Wc, int ar, int ac,
@@ -206,23 +206,28 @@ __device__ __forceinline__ T task_rows_fwd_block(const cplx<T>* tw, cplx<T>* lin
     }
     PTY_PROBE_STAMP(1);
     PTY_PROBE_STAMP(2);
+    // exit wave C * P_m * o_j straight from registers into the transform's
+    // first stage (lane b holds n = B*a + b, the stage-1 input order); the
+    // line only serves as the exchange buffer and receives the spectrum in
+    // natural (padded) order; mode m+1's probe row loads are in flight during
+    // mode m's transform
 #pragma unroll
     for (int m = 0; m < MODES; ++m) {
-        if (m > 0) {
+        C pn[A];
+        if (m + 1 < MODES) {
 #pragma unroll
-            for (int a = 0; a < A; ++a) pv[a] = prow[m * WW + B * a + b];
+            for (int a = 0; a < A; ++a) pn[a] = prow[(m + 1) * WW + B * a + b];
         }
         C* line = lines + (m * RT + gi) * LS;
+        group_fft<T, W, false>(
+            line, tw, b, gmask, [&](int n, int a) { return scale(pv[a] * ov[a], checker<T>(r, n)); },
+            [&](int k, int, C v) { line[pad<W>(k)] = v; });
+        if (m + 1 < MODES) {
 #pragma unroll
-        for (int a = 0; a < A; ++a) {
-            const int n = B * a + b;
-            line[pad<W>(n)] = scale(pv[a] * ov[a], checker<T>(r, n));
+            for (int a = 0; a < A; ++a) pv[a] = pn[a];
         }
     }
-    __syncwarp(gmask);
     PTY_PROBE_STAMP(3);
-#pragma unroll 1
-    for (int m = 0; m < MODES; ++m) line_fft<T, W, false>(lines + (m * RT + gi) * LS, tw, b, gmask);
     PTY_PROBE_STAMP(4);
     team_sync<TEAM>(team);
     PTY_PROBE_STAMP(5);
@@ -270,6 +275,19 @@ __device__ __forceinline__ T task_col_fwd(const cplx<T>* tw, cplx<T>* xch, int b
         *mphase ^= 1u;
     }
 #endif
+#if defined(PTY_P2_ASYNC) && !defined(PTY_TMA_LINES)
+    if constexpr (RES) {   // every mode's column line in flight at once: 16-byte cp.async, no registers
+        constexpr int NCH = W * (int)sizeof(C) / 16;
+        for (int m = 0; m < M; ++m) {
+            const char* src = reinterpret_cast<const char*>(pos + m * WW + (size_t)kc * W);
+            char* dst = reinterpret_cast<char*>(res + m * xch_size<W>());
+#pragma unroll
+            for (int q = b; q < NCH; q += B) cp_async<16>(dst + 16 * q, src + 16 * q);
+        }
+        cp_async_wait_all();
+        __syncwarp(gmask);
+    }
+#endif
 #if defined(PTY_P2_PREFETCH) && !defined(PTY_TMA_LINES)
     C nxt[A];
     if constexpr (RES) {
@@ -301,7 +319,7 @@ __device__ __forceinline__ T task_col_fwd(const cplx<T>* tw, cplx<T>* xch, int b
         if constexpr (RES) {   // Psi_m stays in this group's shared-memory line for P3
             C* rl = res + m * xch_size<W>();
             group_fft<T, W, false>(
-#ifdef PTY_TMA_LINES
+#if defined(PTY_TMA_LINES) || defined(PTY_P2_ASYNC)
                 rl, tw, b, gmask, [&](int n, int) { return rl[n]; },
 #else
                 rl, tw, b, gmask, [&](int n, int) { return line[n]; },
