@@ -51,7 +51,8 @@ struct BatchDev {
     // workspace
     int* anchors;                      // [b][2]
     void* scratch;                     // [b][M][W][W] complex
-    void* onum;                        // [b][M][W][W] complex: per-mode object numerators
+    void* onum;                        // [b][onum_planes][W][W] complex: object numerators
+    int onum_planes;                   // M (per-mode, bk_rows_inv) or 1 (mode sum, the line-task flavour)
     void* pp;                          // [W][W] real (probe power)
     void* pp_part;                     // [nRT] real
     void* omax_part;                   // [b][W/4] real (per row quad)
@@ -359,7 +360,7 @@ __global__ void __launch_bounds__(256) bk_obj_gather(const __grid_constant__ Bat
         return;
     }
     const T gamma = T(P.gamma);
-    const C* onum = reinterpret_cast<const C*>(P.onum);      // [k][m][W][W]
+    const C* onum = reinterpret_cast<const C*>(P.onum);      // [k][onum_planes][W][W]
     T* acc = reinterpret_cast<T*>(P.obj_acc);
     const size_t HW = (size_t)P.H * P.Wc;
     const size_t WW = (size_t)W * W;
@@ -383,15 +384,15 @@ __global__ void __launch_bounds__(256) bk_obj_gather(const __grid_constant__ Bat
             const int p = threadIdx.x + q * 256, R = R0 + p / kObjTile, Cc = C0 + p % kObjTile;
             const int r = R - ar, c = Cc - ac;
             if (R < P.H && Cc < P.Wc && r >= 0 && r < W && c >= 0 && c < W) {
-                const C* src = onum + (size_t)k * P.M * WW + (size_t)r * W + c;
-                C v[kMaxBatchModes];                          // every mode's load in flight at once
+                const C* src = onum + (size_t)k * P.onum_planes * WW + (size_t)r * W + c;
+                C v[kMaxBatchModes];                          // every plane's load in flight at once
 #pragma unroll
                 for (int m = 0; m < kMaxBatchModes; ++m)
-                    if (m < P.M) v[m] = src[(size_t)m * WW];
+                    if (m < P.onum_planes) v[m] = src[(size_t)m * WW];
                 C s = v[0];
 #pragma unroll
                 for (int m = 1; m < kMaxBatchModes; ++m)
-                    if (m < P.M) s = s + v[m];               // mode order, as before
+                    if (m < P.onum_planes) s = s + v[m];     // mode order, as before
                 num[q] = num[q] + s;
                 den[q] += gamma * peak + (T(1) - gamma) * pp[(size_t)r * W + c];
             }

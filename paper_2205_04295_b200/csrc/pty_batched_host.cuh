@@ -4,12 +4,30 @@
 #pragma once
 #include "pty_batched.cuh"
 #include "pty_host.cuh"
+#include "pty_sweep_host.cuh"
 
 namespace pty {
+
+// the contribution pass on the line-task sweep kernel (pty_sweep_host.cuh),
+// instantiated in the pty_sweep_*.cu units
+template <typename T, int W> int run_sweep_batched(const BatchedSweepIO& io, cudaStream_t st);
+template <typename T, int W> int sweep_batched_fits(int M, int S);
+
+// Which contribution pass runs (PTY_BATCH_FUSED=0 forces the five-kernel
+// chain): the line-task flavour when the sweep kernel runs slot-local with
+// staged row blocks for this (dtype, W, M) -- S positions in flight, scratch
+// L2-resident, one object-numerator plane per position.
+template <typename T, int W> inline int fused_slots(int M, int chunk) {
+    if (!env_int("PTY_BATCH_FUSED", 1) || M > 4) return 0;
+    const int S = std::min(batched_max_slots<W>(), chunk);
+    return sweep_batched_fits<T, W>(M, S) ? S : 0;
+}
 
 struct BatchLayout {
     int* anchors;
     void *scratch, *onum, *totT, *pp, *pp_part, *omax_part, *tmax_part, *pgroup, *tile_max, *upd;
+    void* sweep_ws;                    // line-task flavour: the sweep kernel's workspace
+    size_t sweep_ws_bytes;
     size_t bytes;
 };
 
@@ -53,32 +71,49 @@ inline BatchShape batch_shape(int W, int b, int H, int Wc, int G, int chunk) {
 }
 
 template <typename T>
-inline BatchLayout carve_batch(void* ws, int W, int M, int b, const BatchShape& sh, int H, int Wc, bool upd) {
+inline BatchLayout carve_batch(void* ws, int W, int M, int b, const BatchShape& sh, int H, int Wc, bool upd,
+                               int fused_S = 0) {
     Carver c(ws);
     BatchLayout L{};
     const size_t WW = (size_t)W * W;
+    const size_t per = fused_S ? 0 : (size_t)sh.chunk;       // five-kernel chain only
     L.anchors = c.take<int>((size_t)b * 2 * sizeof(int));
-    L.scratch = c.take<void>((size_t)sh.chunk * M * WW * sizeof(cplx<T>));
-    L.onum = c.take<void>((size_t)sh.chunk * M * WW * sizeof(cplx<T>));
-    L.totT = c.take<void>((size_t)sh.chunk * WW * sizeof(T));
+    L.scratch = c.take<void>(per * M * WW * sizeof(cplx<T>));
+    L.onum = c.take<void>((size_t)sh.chunk * (fused_S ? 1 : M) * WW * sizeof(cplx<T>));
+    L.totT = c.take<void>(per * WW * sizeof(T));
     L.pp = c.take<void>(WW * sizeof(T));
     L.pp_part = c.take<void>((size_t)sh.nRT * sizeof(T));
-    L.omax_part = c.take<void>((size_t)sh.chunk * (W / 4) * sizeof(T));
-    L.tmax_part = c.take<void>((size_t)sh.chunk * W * sizeof(T));
+    L.omax_part = c.take<void>(per * (W / 4) * sizeof(T));
+    L.tmax_part = c.take<void>(per * W * sizeof(T));
     L.pgroup = c.take<void>((size_t)sh.G * (2 * M + 1) * WW * sizeof(T));
+    L.sweep_ws_bytes = fused_S ? sweep_batched_workspace<T>(W, M, fused_S, sh.chunk) : 0;
+    L.sweep_ws = c.take<void>(L.sweep_ws_bytes);
     L.tile_max = c.take<void>((size_t)sh.ntiles * sizeof(T));
     L.upd = upd ? c.take<void>((size_t)H * Wc * sizeof(cplx<T>)) : nullptr;
     L.bytes = c.off;
     return L;
 }
 
+// chunking, groups and contribution flavour of a batch (the same answer for
+// the workspace query and the run)
 template <typename T, int W>
-int fill_batch(const PtyBatchArgs* a, BatchDev& P, BatchShape& sh, cudaStream_t st) {
+BatchShape batch_plan(int M, int b, int H, int Wc, int& fused_S) {
+    const int chunk_f = batch_chunk(b, (size_t)W * W * sizeof(cplx<T>));
+    fused_S = fused_slots<T, W>(M, chunk_f);
+    const int chunk = fused_S ? chunk_f : batch_chunk(b, batch_pos_bytes<T>(W, M));
+    return batch_shape(W, b, H, Wc, fused_S ? fused_S : k4_groups<W>(chunk), chunk);
+}
+
+template <typename T, int W>
+int fill_batch(const PtyBatchArgs* a, BatchDev& P, BatchShape& sh, cudaStream_t st, BatchLayout* Lout = nullptr,
+               int* fused_out = nullptr) {
     const int M = a->modes, b = a->n_batch;
-    const int chunk = batch_chunk(b, batch_pos_bytes<T>(W, M));
-    sh = batch_shape(W, b, a->H, a->Wc, k4_groups<W>(chunk), chunk);
+    int fused_S = 0;
+    sh = batch_plan<T, W>(M, b, a->H, a->Wc, fused_S);
     const bool upd = a->sense == PTY_SENSE_XCORR_A;
-    BatchLayout L = carve_batch<T>(a->workspace, W, M, b, sh, a->H, a->Wc, upd);
+    BatchLayout L = carve_batch<T>(a->workspace, W, M, b, sh, a->H, a->Wc, upd, fused_S);
+    if (Lout) *Lout = L;
+    if (fused_out) *fused_out = fused_S;
     if (!a->workspace || a->workspace_bytes < (int64_t)L.bytes) return PTY_ERR_ARGUMENT;
     P = BatchDev{};
     P.W = W; P.M = M; P.N = a->n_positions; P.b = b;
@@ -92,6 +127,7 @@ int fill_batch(const PtyBatchArgs* a, BatchDev& P, BatchShape& sh, cudaStream_t 
     P.stage = a->stage; P.obj_acc = a->obj_acc; P.probe_acc = a->probe_acc;
     P.err_part = a->err_part; P.status = a->status;
     P.anchors = L.anchors; P.scratch = L.scratch; P.onum = L.onum; P.totT = L.totT; P.pp = L.pp;
+    P.onum_planes = fused_S ? 1 : M;
     P.pp_part = L.pp_part; P.omax_part = L.omax_part; P.tmax_part = L.tmax_part; P.pgroup = L.pgroup;
     P.tile_max = L.tile_max; P.upd = L.upd;
     P.twiddles = twiddles<T, W>(st);
@@ -113,12 +149,47 @@ template <typename K> inline int persistent_grid(K kern, int threads, size_t sme
 }
 
 template <typename T, int W>
+int run_batch_contrib_fused(const PtyBatchArgs* a, BatchDev& P, const BatchShape& sh, const BatchLayout& L, int S,
+                            cudaStream_t st) {
+    const int M = a->modes, b = a->n_batch;
+    const size_t s_gather = (size_t)sh.chunk * sizeof(int);
+    if (s_gather > max_dyn_smem()) return PTY_ERR_ARGUMENT;
+    int rc = set_smem(bk_obj_gather<T, W>, s_gather);
+    if (rc) return rc;
+    const size_t HW = (size_t)a->H * a->Wc, WW = (size_t)W * W;
+    cudaMemsetAsync(a->obj_acc, 0, 3 * HW * sizeof(T), st);
+    cudaMemsetAsync(a->probe_acc, 0, (size_t)(2 * M + 1) * WW * sizeof(T), st);
+    cudaMemsetAsync(L.pgroup, 0, (size_t)S * (2 * M + 1) * WW * sizeof(T), st);
+    bk_probe_power<T, W><<<std::max(sh.nRT, (b + kBatThreads - 1) / kBatThreads), kBatThreads, 0, st>>>(P);
+    int launches = 1;
+    for (int off = 0; off < b; off += sh.chunk) {   // the batch in chunks, in order
+        BatchedSweepIO io{a, off, std::min(sh.chunk, b - off), S, L.onum, L.pgroup, L.sweep_ws, L.sweep_ws_bytes};
+        rc = run_sweep_batched<T, W>(io, st);
+        if (rc) return rc == kBatchedNoFit ? PTY_ERR_ARGUMENT : rc;
+        BatchDev Q = P;
+        Q.b = io.cnt;
+        Q.batch = P.batch + off;
+        Q.anchors = P.anchors + 2 * off;
+        Q.visit0 = P.visit0 + off;
+        bk_obj_gather<T, W><<<sh.ntiles, 256, s_gather, st>>>(Q);
+        launches += 1;
+    }
+    P.G = S;
+    bk_probe_reduce<T, W><<<std::min<size_t>(4096, ((2 * M + 1) * WW + 255) / 256), 256, 0, st>>>(P);
+    count(launches + 1);
+    return last_status();
+}
+
+template <typename T, int W>
 int run_batch_contrib(const PtyBatchArgs* a, cudaStream_t st) {
     BatchDev P;
     BatchShape sh;
-    int rc = fill_batch<T, W>(a, P, sh, st);
+    BatchLayout L;
+    int fused_S = 0;
+    int rc = fill_batch<T, W>(a, P, sh, st, &L, &fused_S);
     if (rc) return rc;
     if (!a->patterns_t) return PTY_ERR_ARGUMENT;
+    if (fused_S) return run_batch_contrib_fused<T, W>(a, P, sh, L, fused_S, st);
     const int M = a->modes, b = a->n_batch;
     constexpr int B = Shape<W>::B, TEAM = 4 * B, NTEAM = kLineThreads / TEAM, XS = xch_size<W>();
     constexpr int LS4 = team_line_stride<W>();
@@ -188,9 +259,9 @@ int run_batch_apply(const PtyBatchArgs* a, cudaStream_t st) {
 
 template <typename T, int W>
 int64_t batch_workspace(int M, int b, int H, int Wc, bool upd) {
-    const int chunk = batch_chunk(b, batch_pos_bytes<T>(W, M));
-    BatchShape sh = batch_shape(W, b, H, Wc, k4_groups<W>(chunk), chunk);
-    return (int64_t)carve_batch<T>(nullptr, W, M, b, sh, H, Wc, upd).bytes;
+    int fused_S = 0;
+    BatchShape sh = batch_plan<T, W>(M, b, H, Wc, fused_S);
+    return (int64_t)carve_batch<T>(nullptr, W, M, b, sh, H, Wc, upd, fused_S).bytes;
 }
 
 }  // namespace pty

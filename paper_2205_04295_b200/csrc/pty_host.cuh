@@ -63,6 +63,41 @@ inline int env_int(const char* name, int dflt) {
     return v ? std::atoi(v) : dflt;
 }
 
+// L2 persistence window over a kernel's scratch (PTY_L2_PERSIST_MB > 0): the
+// line-task kernels rewrite their scratch every phase; streaming inputs and
+// outputs (patterns, object patches, numerator planes) would otherwise evict
+// it between the write and the read.  Returns whether a window was set.
+inline bool l2_window_set(cudaStream_t st, void* base, size_t bytes) {
+    const int mb = env_int("PTY_L2_PERSIST_MB", 0);
+    if (mb <= 0 || !base || !bytes) return false;
+    static size_t limit = 0;
+    const size_t want = (size_t)mb << 20;
+    if (limit != want) {
+        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        limit = want;
+    }
+    cudaStreamAttrValue v{};
+    v.accessPolicyWindow.base_ptr = base;
+    v.accessPolicyWindow.num_bytes = std::min(bytes, want);
+    v.accessPolicyWindow.hitRatio = 1.0f;
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    if (cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return true;
+}
+inline void l2_window_clear(cudaStream_t st) {
+    cudaStreamAttrValue v{};
+    v.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v);
+    cudaGetLastError();
+}
+
 inline int pow2_floor(int x) {
     int p = 1;
     while (p * 2 <= x) p *= 2;

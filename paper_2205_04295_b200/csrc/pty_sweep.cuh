@@ -64,7 +64,7 @@ struct SweepDev {
     int4* steptab;                // [nslots][N]: (j, ar, ac, 0) of visit step t (order[t] and its anchor)
     void* scratch;                // [nslots][M][W][W] complex, transposed after the row pass
     void* totT;                   // [nslots][W][W] real
-    void* omax_part;              // [nslots][W/4] real
+    void* omax_part;              // [2][nslots][W/4] real (by step parity)
     void* peak_part;              // [2][nslots][W/4] real
     void* tmax_part;              // [nslots][W] real
     double* err_part;             // [nslots][N][W][3] per-visit, per-column error terms
@@ -72,6 +72,15 @@ struct SweepDev {
     const void* twiddles;         // [W] complex, global
     unsigned long long* timeline; // debug: [steps][9][gridDim] globaltimer stamps or null
     int timeline_steps;
+    // batched extension (oracle/batched.py contrib): slot s takes batch
+    // positions k = s, s + nslots, ... (steptab (j, ar, ac, k), j < 0: idle
+    // step); object and probes stay at the batch start; the P4->P1 barrier is
+    // not needed (nothing a next step reads is written in P4)
+    int batched;
+    int visit0;                   // visit rank of batch position 0 (err_batch index)
+    void* onum;                   // [b][W][W] complex: per-position object numerator
+    void* pgroup;                 // [nslots][2M+1][W][W] real: per-slot probe numerators / denominator
+    double* err_batch;            // [N_dataset][W][3] by visit rank
     SlotDev slot[kMaxSlots];
 };
 
@@ -164,14 +173,14 @@ __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-template <typename T, int W, bool CL>
+template <typename T, int W, bool CL, bool BAT = false>
 __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kernel(const __grid_constant__ SweepDev P) {
     using C = cplx<T>;
     constexpr int B = Shape<W>::B, TEAM = 4 * B, XS = xch_size<W>(), LS4 = team_line_stride<W>();
     constexpr int NTEAM = kSweepThreads / TEAM, NGRP = kSweepThreads / B;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // per-step snapshot of every slot: dead flag, position index, anchor
-    __shared__ int s_dead[kMaxSlots], s_j[kMaxSlots], s_ar[kMaxSlots], s_ac[kMaxSlots];
+    __shared__ int s_dead[kMaxSlots], s_j[kMaxSlots], s_ar[kMaxSlots], s_ac[kMaxSlots], s_k[kMaxSlots];
     __shared__ unsigned long long s_mbar[NGRP];               // one bulk-copy barrier per line group
     unsigned mphase = 0u;                                      // its parity (identical on the group's lanes)
     C* tw = reinterpret_cast<C*>(smem_raw);
@@ -258,7 +267,7 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
     __syncthreads();
 
     // ---- phase 0: anchors (engine.py:69-70, 192-195) + bounds, initial probe peak
-    for (int li = cta * NT + tid; li < S * N; li += ncta * NT) {
+    for (int li = cta * NT + tid; li < (BAT ? 0 : S * N); li += ncta * NT) {
         const int idx = s0 * N + li;
         const int s = idx / N, j = idx % N;
         const SlotDev& sl = P.slot[s];
@@ -364,6 +373,7 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
             s_j[s] = v.x;
             s_ar[s] = v.y;
             s_ac[s] = v.z;
+            s_k[s] = v.x < 0 ? -1 : v.w;                         // batched: -1 = no position this step
         }
         __syncthreads();
         // ---------------------------------------------------------- P1 rows
@@ -372,7 +382,7 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
             T* red_s = reinterpret_cast<T*>(reinterpret_cast<C*>(region) + (size_t)NTEAM_S * M * RTS * LSS) + team_s * RTS;
             for (int task = vcta * NTEAM_S + team_s; task < S * nq; task += ncta * NTEAM_S) {
                 const int s = s0 + task / nq, rq = task % nq;
-                if (s_dead[s]) continue;
+                if (s_dead[s] | (s_k[s] < 0)) continue;
                 const SlotDev& sl = P.slot[s];
                 const int j = s_j[s];
                 const char* It = reinterpret_cast<const char*>(reinterpret_cast<const T*>(sl.patterns_t) + (size_t)j * WW +
@@ -391,12 +401,12 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
                     default: PTY_P1S(4); break;
                 }
 #undef PTY_P1S
-                if (tl_s == 0) omax_part[(size_t)s * nq + rq] = om;
+                if (tl_s == 0) omax_part[((size_t)(step & 1) * P.nslots + s) * nq + rq] = om;
             }
         } else
         for (int task = vcta * NTEAM + team; task < S * M * nq; task += ncta * NTEAM) {
             const int s = s0 + task / (M * nq), m = (task / nq) % M, rq = task % nq;
-            if (s_dead[s]) continue;
+            if (s_dead[s] | (s_k[s] < 0)) continue;
             const SlotDev& sl = P.slot[s];
             const int j = s_j[s];
             // this visit's pattern column lines P3 will read: HBM -> L2
@@ -410,7 +420,7 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
             const T om = task_row_fwd<T, W>(tw, xch, tt, red4_p1, team, tl, gi, b, gmask,
                                             reinterpret_cast<const C*>(sl.obj), sl.Wc, s_ar[s], s_ac[s],
                                             reinterpret_cast<const C*>(sl.probes), m, rq, scratch + (size_t)s * M * WW, stg);
-            if (m == 0 && tl == 0) omax_part[(size_t)s * nq + rq] = om;
+            if (m == 0 && tl == 0) omax_part[((size_t)(step & 1) * P.nslots + s) * nq + rq] = om;
         }
         stamp(step, 1);
         phase_sync();
@@ -418,7 +428,7 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
         // ------------------------------------------------- P2 cols (forward)
         for (int task = vcta * NGRP + grp; task < S * W; task += ncta * NGRP) {
             const int s = s0 + task / W, kc = task % W;
-            if (s_dead[s]) continue;
+            if (s_dead[s] | (s_k[s] < 0)) continue;
             const T tm = P.resident
                 ? task_col_fwd<T, W, true>(tw, xch, b, gmask, scratch + (size_t)s * M * WW, M, kc, totT + (size_t)s * WW, res,
                                            &s_mbar[grp], &mphase)
@@ -431,12 +441,13 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
         // ---------------------------------------- P3 modulus + cols (inverse)
         for (int task = vcta * NGRP + grp; task < S * W; task += ncta * NGRP) {
             const int s = s0 + task / W, kc = task % W;
-            if (s_dead[s]) continue;
+            if (s_dead[s] | (s_k[s] < 0)) continue;
             const SlotDev& sl = P.slot[s];
             const int j = s_j[s];
             C* stg = P.sense == PTY_SENSE_XCORR_B ? reinterpret_cast<C*>(sl.stage) + (size_t)j * 2 * WW : nullptr;
             const T* It = reinterpret_cast<const T*>(sl.patterns_t) + (size_t)j * WW;
-            double* ep = P.err_part + (((size_t)s * N + step) * W + kc) * 3;
+            double* ep = BAT ? P.err_batch + ((size_t)(P.visit0 + s_k[s]) * W + kc) * 3
+                                   : P.err_part + (((size_t)s * N + step) * W + kc) * 3;
             if (P.resident)
                 task_col_mod<T, W, true>(tw, xch, b, gmask, scratch + (size_t)s * M * WW, M, kc, totT + (size_t)s * WW,
                                          tmax_part + (size_t)s * W, It, T(P.eps_rel), P.track_mod, stg, ep, res);
@@ -453,17 +464,34 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
             T* red_s = reinterpret_cast<T*>(reinterpret_cast<C*>(region) + (size_t)NTEAM_S * M * RTS * LSS) + team_s * RTS;
             for (int task = vcta * NTEAM_S + team_s; task < S * nq; task += ncta * NTEAM_S) {
                 const int s = s0 + task / nq, rq = task % nq;
-                if (s_dead[s]) continue;
+                if (s_dead[s] | (s_k[s] < 0)) continue;
                 const SlotDev& sl = P.slot[s];
                 const int j = s_j[s];
                 // the maxima partials are reduced inside the task, while the
                 // block's scratch rows are already in flight (engine.py:132-134,
                 // 145-147 checked there: a failing slot returns its error bit)
-                const T* pkp = peak_part + ((size_t)(step & 1) * P.nslots + s) * nq;
-                const T* omp = omax_part + (size_t)s * nq;
+                const T* pkp = peak_part + ((size_t)(BAT ? 0 : step & 1) * P.nslots + s) * nq;
+                const T* omp = omax_part + ((size_t)(step & 1) * P.nslots + s) * nq;
+                int bad = 0;
+                if constexpr (BAT) {
+#define PTY_P4A(MM) task_rows_acc_block<T, W, MM, RTS>(tw, lines_m, team_s, tl_s, gi_s, b, gmask, \
+                    scratch + (size_t)s * M * WW, rq, reinterpret_cast<const C*>(sl.obj), sl.Wc, s_ar[s], s_ac[s], \
+                    reinterpret_cast<const C*>(sl.probes), pkp, omp, nq, U, reinterpret_cast<C*>(P.onum) + (size_t)s_k[s] * WW, \
+                    reinterpret_cast<T*>(P.pgroup) + (size_t)s * (2 * M + 1) * WW, bad)
+                    switch (M) {
+                        case 1: PTY_P4A(1); break;
+                        case 2: PTY_P4A(2); break;
+                        case 3: PTY_P4A(3); break;
+                        default: PTY_P4A(4); break;
+                    }
+#undef PTY_P4A
+                    if (bad) {
+                        if (tl_s == 0) atomicOr(sl.status, bad);
+                        if (local && tid == 0) s_dead[s] = 1;
+                    }
+                } else {
                 C* stg = P.sense == PTY_SENSE_XCORR_A ? reinterpret_cast<C*>(sl.stage) + (size_t)j * 2 * WW : nullptr;
                 T npk;
-                int bad = 0;
 #define PTY_P4S(MM) npk = task_rows_inv_block<T, W, MM, RTS>(tw, lines_m, red_s, team_s, tl_s, gi_s, b, gmask, \
                     scratch + (size_t)s * M * WW, rq, reinterpret_cast<C*>(sl.obj), reinterpret_cast<T*>(P.ppg) + (size_t)s * WW, \
                     sl.Wc, s_ar[s], s_ac[s], reinterpret_cast<C*>(sl.probes), pkp, omp, nq, U, stg, bad)
@@ -480,15 +508,16 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
                     continue;
                 }
                 if (tl_s == 0) peak_part[((size_t)((step + 1) & 1) * P.nslots + s) * nq + rq] = npk;
+                }
             }
-        } else
+        } else if constexpr (!BAT)                            // the batched flavour runs staged only
         for (int task = vcta * NTEAM + team; task < S * nq; task += ncta * NTEAM) {
             const int s = s0 + task / nq, rq = task % nq;
-            if (s_dead[s]) continue;
+            if (s_dead[s] | (s_k[s] < 0)) continue;
             const SlotDev& sl = P.slot[s];
             const int j = s_j[s];
             const T* pkp = peak_part + ((size_t)(step & 1) * P.nslots + s) * nq;
-            const T* omp = omax_part + (size_t)s * nq;
+            const T* omp = omax_part + ((size_t)(step & 1) * P.nslots + s) * nq;
             T peak = T(0), omax = T(0);
 #pragma unroll
             for (int q = b; q < nq; q += B) {
@@ -511,7 +540,7 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepMaxCtasPerSm) sweep_kerne
             if (tl == 0) peak_part[((size_t)((step + 1) & 1) * P.nslots + s) * nq + rq] = npk;
         }
         stamp(step, 7);
-        phase_sync();
+        if constexpr (!BAT) phase_sync();
         stamp(step, 8);
         if (P.timeline && step == 0 && tid == 0) {      // debug: the CTA's SM id replaces stamp (0, 8)
             unsigned sm;

@@ -2,4 +2,6 @@
 #include "pty_sweep_host.cuh"
 namespace pty {
 template int run_sweep<float, 16>(const PtySweepArgs*, cudaStream_t);
+template int run_sweep_batched<float, 16>(const BatchedSweepIO&, cudaStream_t);
+template int sweep_batched_fits<float, 16>(int, int);
 }

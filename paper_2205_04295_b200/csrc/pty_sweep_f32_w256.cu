@@ -2,6 +2,8 @@
 #include "pty_sweep_host.cuh"
 namespace pty {
 template int run_sweep<float, 256>(const PtySweepArgs*, cudaStream_t);
+template int run_sweep_batched<float, 256>(const BatchedSweepIO&, cudaStream_t);
+template int sweep_batched_fits<float, 256>(int, int);
 }
 
 #ifdef PTY_PROBE

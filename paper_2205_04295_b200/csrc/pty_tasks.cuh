@@ -598,36 +598,20 @@ __device__ __forceinline__ bool block_maxima(const T* peak_part, const T* omax_p
     return true;
 }
 
-// Row pass 2, staged variant (shared memory for all modes): team task (row
-// quad rq) of one position.  (1) the 4 rows of every mode are loaded into the
-// team's lines (lines[(m*4 + gi)*LS4 + pad(c)]), (2) every line is
-// inverse-transformed in place, (3) the update epilogue runs element-linear
-// over the team with all of an element's inputs (o, sum|P|^2, P_m, psi'_m)
-// gathered first and its accumulators in registers.  Same expressions and
-// mode order as task_row_inv_update (engine.py:119-150, 218-224,
-// fields.py:101-107).  Returns the team max of the next visit's sum_m |P_m|^2.
+// The block's scratch rows ([m][kc][RT*blk + row]: RT consecutive complex
+// values per column -- a 128-byte line for RT = 16) of every mode into the
+// team's lines (lines[(m*RT + row)*LS + pad(kc)]) and their inverse row
+// transforms in place; this visit's maxima come from their per-block partials
+// while the rows are in flight.  false (and the error bit in `bad`) if the
+// update is degenerate -- uniform over the team, no shared memory touched.
 template <typename T, int W, int MODES, int RT>
-__device__ __forceinline__ T task_rows_inv_block(const cplx<T>* tw, cplx<T>* lines, T* red, int team,
-                                                 int tl, int gi, int b, unsigned gmask, const cplx<T>* pos,
-                                                 int blk, cplx<T>* obj, T* ppg, int Wc, int ar, int ac,
-                                                 cplx<T>* probes, const T* peak_part, const T* omax_part, int nparts,
-                                                 const UpdateParams& U, cplx<T>* stg, int& bad) {
+__device__ __forceinline__ bool stage_inverse_rows(const cplx<T>* tw, cplx<T>* lines, int team, int tl, int gi, int b,
+                                                   unsigned gmask, const cplx<T>* pos, int blk, const T* peak_part,
+                                                   const T* omax_part, int nparts, int update_probe, T& peak, T& omax,
+                                                   int& bad) {
     using C = cplx<T>;
     constexpr int B = Shape<W>::B, TEAM = RT * B, LS = block_line_stride<W, RT>(), NE = RT * W / TEAM;
-#ifdef PTY_P4_CH
-    constexpr int CH = MODES <= 3 ? PTY_P4_CH : (MODES <= 6 ? 2 : 1);
-#else
-    constexpr int CH = MODES <= 3 ? 4 : (MODES <= 6 ? 2 : 1);
-#endif
     const size_t WW = (size_t)W * W;
-    const T invW2 = T(1) / (T(W) * T(W));
-    const T alpha_o = T(U.alpha_o), alpha_p = T(U.alpha_p), beta = T(U.beta), gamma = T(U.gamma),
-            eps_rel = T(U.eps_rel);
-    T peak, omax;
-    PTY_PROBE_STAMP(10);
-    // the block's scratch rows ([m][kc][RT*blk + row]: RT consecutive complex
-    // values per column -- a 128-byte line for RT = 16) into the team's lines;
-    // mode m+1's loads are in flight while mode m is stored to shared memory
 #ifndef PTY_P4_REGS
     // every mode's rows in flight at once (cp.async, no register staging;
     // PTY_P4_REGS: the register-staged loads, mode m+1 in flight while mode m
@@ -642,9 +626,9 @@ __device__ __forceinline__ T task_rows_inv_block(const cplx<T>* tw, cplx<T>* lin
                                 pos + m * WW + (size_t)(e / RT) * W + RT * blk + (e % RT));
         }
     }
-    if (!block_maxima<T, B>(peak_part, omax_part, nparts, b, U.update_probe, peak, omax, bad)) {
+    if (!block_maxima<T, B>(peak_part, omax_part, nparts, b, update_probe, peak, omax, bad)) {
         cp_async_wait_all();
-        return T(0);
+        return false;
     }
     cp_async_wait_all();
 #else
@@ -654,7 +638,7 @@ __device__ __forceinline__ T task_rows_inv_block(const cplx<T>* tw, cplx<T>* lin
         const int e = tl + i * TEAM;
         cur[i] = pos[(size_t)(e / RT) * W + RT * blk + (e % RT)];
     }
-    if (!block_maxima<T, B>(peak_part, omax_part, nparts, b, U.update_probe, peak, omax, bad)) return T(0);
+    if (!block_maxima<T, B>(peak_part, omax_part, nparts, b, update_probe, peak, omax, bad)) return false;
     team_sync<TEAM>(team);                                     // lines free
 #pragma unroll
     for (int m = 0; m < MODES; ++m) {
@@ -683,6 +667,42 @@ __device__ __forceinline__ T task_rows_inv_block(const cplx<T>* tw, cplx<T>* lin
     PTY_PROBE_STAMP(12);
     team_sync<TEAM>(team);
     PTY_PROBE_STAMP(13);
+    return true;
+}
+
+// Row pass 2, staged variant (shared memory for all modes): team task (block
+// blk of RT rows) of one position.  (1) stage_inverse_rows brings every mode's
+// rows into the team's lines and inverse-transforms them in place, (2) the
+// update epilogue runs element-linear over the team with all of an element's
+// inputs (o, sum|P|^2, P_m, psi'_m) gathered first and its accumulators in
+// registers.  Same expressions and mode order as task_row_inv_update
+// (engine.py:119-150, 218-224, fields.py:101-107).  Returns the team max of
+// the next visit's sum_m |P_m|^2.
+template <typename T, int W, int MODES, int RT>
+__device__ __forceinline__ T task_rows_inv_block(const cplx<T>* tw, cplx<T>* lines, T* red, int team,
+                                                 int tl, int gi, int b, unsigned gmask, const cplx<T>* pos,
+                                                 int blk, cplx<T>* obj, T* ppg, int Wc, int ar, int ac,
+                                                 cplx<T>* probes, const T* peak_part, const T* omax_part, int nparts,
+                                                 const UpdateParams& U, cplx<T>* stg, int& bad) {
+    using C = cplx<T>;
+    constexpr int B = Shape<W>::B, TEAM = RT * B, LS = block_line_stride<W, RT>(), NE = RT * W / TEAM;
+#ifdef PTY_P4_CH
+    constexpr int CH = MODES <= 3 ? PTY_P4_CH : (MODES <= 6 ? 2 : 1);
+#else
+    constexpr int CH = MODES <= 3 ? 4 : (MODES <= 6 ? 2 : 1);
+#endif
+    const size_t WW = (size_t)W * W;
+    const T invW2 = T(1) / (T(W) * T(W));
+    const T alpha_o = T(U.alpha_o), alpha_p = T(U.alpha_p), beta = T(U.beta), gamma = T(U.gamma),
+            eps_rel = T(U.eps_rel);
+    T peak, omax;
+    PTY_PROBE_STAMP(10);
+    // the block's scratch rows ([m][kc][RT*blk + row]: RT consecutive complex
+    // values per column -- a 128-byte line for RT = 16) into the team's lines;
+    // mode m+1's loads are in flight while mode m is stored to shared memory
+    if (!stage_inverse_rows<T, W, MODES, RT>(tw, lines, team, tl, gi, b, gmask, pos, blk, peak_part, omax_part, nparts,
+                                             U.update_probe, peak, omax, bad))
+        return T(0);
     const T dmax_p = beta * omax + (T(1) - beta) * omax;
     const T dmax_o = gamma * peak + (T(1) - gamma) * peak;
     T pk = T(0);
@@ -744,6 +764,70 @@ __device__ __forceinline__ T task_rows_inv_block(const cplx<T>* tw, cplx<T>* lin
     PTY_PROBE_STAMP(14);
     pk = group_max<B>(pk);
     return team_maxn<W, RT>(pk, red, team, gi, b);
+}
+
+// Row pass 2 of the batched extension (oracle/batched.py contrib; the
+// reference has no batched mode): same staging and inverse
+// transforms as task_rows_inv_block, but nothing is written back -- every
+// position of a batch sees the batch-start object and probes.  Per element the
+// position's object numerator sum_m (psi'_m - P_m o) conj(P_m) (engine.py:
+// 130-131) goes to its own plane onum_k, and the probe numerators alpha_P
+// (psi'_m - P_m o) conj(o) (engine.py:150) and denominator beta max|o|^2 +
+// (1 - beta)|o|^2 (engine.py:148) are added into this slot's group
+// accumulator pg ([2M+1][W][W] real: re/im per mode, then the denominator,
+// zeroed per batch).  The rows of block blk of pg are added to by this team
+// alone, position after position, with fire-and-forget reductions (red.add:
+// no load round trip; same-thread same-address order = the slot's batch
+// order, so the sums are deterministic and equal the load-add-store ones).
+template <typename T, int W, int MODES, int RT>
+__device__ __forceinline__ void task_rows_acc_block(const cplx<T>* tw, cplx<T>* lines, int team, int tl, int gi, int b,
+                                                    unsigned gmask, const cplx<T>* pos, int blk, const cplx<T>* obj,
+                                                    int Wc, int ar, int ac, const cplx<T>* probes, const T* peak_part,
+                                                    const T* omax_part, int nparts, const UpdateParams& U,
+                                                    cplx<T>* onum_k, T* pg, int& bad) {
+    using C = cplx<T>;
+    constexpr int B = Shape<W>::B, TEAM = RT * B, LS = block_line_stride<W, RT>(), NE = RT * W / TEAM;
+    constexpr int CH = MODES <= 3 ? 4 : (MODES <= 6 ? 2 : 1);
+    const size_t WW = (size_t)W * W;
+    const T invW2 = T(1) / (T(W) * T(W));
+    const T alpha_p = T(U.alpha_p), beta = T(U.beta);
+    T peak, omax;
+    if (!stage_inverse_rows<T, W, MODES, RT>(tw, lines, team, tl, gi, b, gmask, pos, blk, peak_part, omax_part, nparts,
+                                             U.update_probe, peak, omax, bad))
+        return;
+#pragma unroll 1
+    for (int h = 0; h < NE; h += CH) {
+        C ov[CH], pv[MODES][CH];
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+            const int e = tl + (h + k) * TEAM, rr = e / W, c = e % W, r = RT * blk + rr;
+            ov[k] = obj[(size_t)(ar + r) * Wc + ac + c];
+#pragma unroll
+            for (int m = 0; m < MODES; ++m) pv[m][k] = probes[m * WW + (size_t)r * W + c];
+        }
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+            const int e = tl + (h + k) * TEAM, rr = e / W, c = e % W, r = RT * blk + rr;
+            const size_t off = (size_t)r * W + c;
+            const C o = ov[k];
+            const OMul<T> om(o);
+            C numer{T(0), T(0)};
+#pragma unroll
+            for (int m = 0; m < MODES; ++m) {
+                const C X = lines[(m * RT + rr) * LS + pad<W>(c)];
+                const C d = scale(X, checker<T>(r, c) * invW2) - om.mul(pv[m][k]);
+                numer = numer + mulc(d, pv[m][k]);
+                if (U.update_probe) {
+                    const C pn = om.mulconj(scale(d, alpha_p));
+                    atomicAdd(pg + (2 * m) * WW + off, pn.re);
+                    atomicAdd(pg + (2 * m + 1) * WW + off, pn.im);
+                }
+            }
+            onum_k[off] = numer;
+            if (U.update_probe) atomicAdd(pg + (2 * MODES) * WW + off, beta * omax + (T(1) - beta) * norm2(o));
+        }
+    }
+    team_sync<TEAM>(team);                                     // lines free for the next task
 }
 
 }  // namespace pty

@@ -157,3 +157,28 @@ def test_batched_memory_budget_chunks_automatically(gpu, monkeypatch):
     e = batched_case(64, 2, (4, 4), 16, "fp64", step=12.0)
     report("batched W64 b16 budget-chunked", [e])
     assert e[0] < FP64_TOL and e[1] < FP64_TOL
+
+
+def test_batched_line_task_flavour_vs_chain_and_oracle(gpu, monkeypatch):
+    """The batched contribution pass on the line-task sweep kernel (default
+    where it fits: 18 positions in flight, one object-numerator plane per
+    position, slot groups for the probe terms) against the five-kernel chain
+    (PTY_BATCH_FUSED=0) and the oracle: 25 positions in one batch of 40 (two
+    slot steps, the second one short), fp32 and fp64.  The launch counts show
+    which pass ran (fp64 at W = 256 takes the chain: its staged row blocks do
+    not fit in shared memory)."""
+    from paper_2205_04295_b200 import _native
+    for precision, tol in (("fp32", FP32_TOL), ("fp64", FP64_TOL)):
+        res = {}
+        batched_case(256, 3, (5, 5), 40, precision, sweeps=1)      # one-time launches (twiddle tables)
+        for fused in ("1", "0"):
+            monkeypatch.setenv("PTY_BATCH_FUSED", fused)
+            n0 = _native.launch_count()
+            e = batched_case(256, 3, (5, 5), 40, precision, sweeps=1)
+            res[fused] = (e, _native.launch_count() - n0)
+            report(f"batched W256 b40 {precision} fused={fused} launches={res[fused][1]}", [e])
+            assert e[0] < tol and e[1] < tol
+        if precision == "fp32":                   # fewer launches: the line-task pass ran
+            assert res["1"][1] < res["0"][1]
+        else:                                     # complex128 row blocks exceed shared memory: the chain
+            assert res["1"][1] == res["0"][1]

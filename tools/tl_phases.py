@@ -25,7 +25,7 @@ act = tl[0, 1, :] > 0                              # CTAs that did work
 tl = tl[:, :, act]
 steps = tl.shape[0]
 task = np.zeros(4); wait = np.zeros(4); crit = np.zeros(4); tmax = np.zeros(4)
-for s_ in range(1, steps - 1):
+for s_ in range(2, steps - 1):   # step 1 stamp 8 carries the virtual CTA index
     for k in range(4):
         start = tl[s_, 2 * k, :]                  # barrier exit of the previous phase (k=0: step start)
         end = tl[s_, 2 * k + 1, :]
@@ -34,7 +34,7 @@ for s_ in range(1, steps - 1):
         tmax[k] += np.mean(np.max(end - start))
         wait[k] += np.mean(ext - end)
         crit[k] += np.max(ext) - np.max(start)
-n = steps - 2
+n = steps - 3
 print("phase        P1     P2     P3     P4   (us, mean over CTAs and steps)")
 print("task mean ", np.round(task / n / 1e3, 2))
 print("task max  ", np.round(tmax / n / 1e3, 2))
