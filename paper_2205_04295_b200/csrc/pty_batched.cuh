@@ -309,11 +309,12 @@ __global__ void bk_probe_reduce(const __grid_constant__ BatchDev P) {
 // Owner-computes object accumulation: CTA = one kObjTile x kObjTile canvas tile;
 // it lists the batch positions covering the tile in batch order (block scan)
 // and sums their numerators and denominators (engine.py:130-136) in that order.
-template <typename T, int W>
+template <typename T, int W, bool ONE_PLANE = false>
 __global__ void __launch_bounds__(256) bk_obj_gather(const __grid_constant__ BatchDev P) {
     using C = cplx<T>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    int* list = reinterpret_cast<int*>(smem_raw);            // [b]
+    int* list = reinterpret_cast<int*>(smem_raw);            // [b] covering positions, batch order
+    int2* lanc = reinterpret_cast<int2*>(list + ((P.b + 1) & ~1));   // [b] their anchors
     __shared__ int wcount[8], total;
     const int tiles_x = (P.Wc + kObjTile - 1) / kObjTile;
     const int ty = blockIdx.x / tiles_x, tx = blockIdx.x % tiles_x;
@@ -326,12 +327,15 @@ __global__ void __launch_bounds__(256) bk_obj_gather(const __grid_constant__ Bat
     constexpr int LR = 8;                                     // list rounds whose anchor loads fly together
     for (int base0 = 0; base0 < P.b; base0 += LR * blockDim.x) {
         bool covr[LR];
+        int2 anc[LR];
 #pragma unroll
         for (int u = 0; u < LR; ++u) {
             const int k = base0 + u * blockDim.x + threadIdx.x;
             covr[u] = false;
+            anc[u] = make_int2(0, 0);
             if (k < P.b) {
                 const int ar = P.anchors[2 * k], ac = P.anchors[2 * k + 1];
+                anc[u] = make_int2(ar, ac);
                 covr[u] = ar < R0 + kObjTile && ar + W > R0 && ac < C0 + kObjTile && ac + W > C0;
             }
         }
@@ -346,7 +350,11 @@ __global__ void __launch_bounds__(256) bk_obj_gather(const __grid_constant__ Bat
             __syncthreads();
             int off = total;
             for (int w = 0; w < wid; ++w) off += wcount[w];
-            if (cov) list[off + __popc(bal & ((1u << lane) - 1u))] = k;
+            if (cov) {
+                const int slot = off + __popc(bal & ((1u << lane) - 1u));
+                list[slot] = k;
+                lanc[slot] = anc[u];
+            }
             __syncthreads();
             if (threadIdx.x == 0) for (int w = 0; w < (int)(blockDim.x >> 5); ++w) total += wcount[w];
             __syncthreads();
@@ -369,37 +377,71 @@ __global__ void __launch_bounds__(256) bk_obj_gather(const __grid_constant__ Bat
     T den[PX];
 #pragma unroll
     for (int q = 0; q < PX; ++q) { num[q] = C{T(0), T(0)}; den[q] = T(0); }
-    // the next covering position's anchors are fetched while this one's
-    // numerators load (one dependent L2 round trip per position instead of two)
-    int k = list[0], ar = P.anchors[2 * k], ac = P.anchors[2 * k + 1];
-    for (int t = 0; t < total; ++t) {
-        int kn = k, arn = ar, acn = ac;
-        if (t + 1 < total) {
-            kn = list[t + 1];
-            arn = P.anchors[2 * kn];
-            acn = P.anchors[2 * kn + 1];
-        }
+    // one numerator plane per position (the line-task pass): covering positions
+    // in batch order, U at a time -- their numerator and sum|P|^2 loads fly
+    // together, the sums are added in list order
+    auto accumulate = [&](auto u_const) {
+        constexpr int U = decltype(u_const)::value;
+        for (int t0 = 0; t0 < total; t0 += U) {
+            C v[U][PX];
+            T pw[U][PX];
+            bool ok[U][PX];
 #pragma unroll
-        for (int q = 0; q < PX; ++q) {
-            const int p = threadIdx.x + q * 256, R = R0 + p / kObjTile, Cc = C0 + p % kObjTile;
-            const int r = R - ar, c = Cc - ac;
-            if (R < P.H && Cc < P.Wc && r >= 0 && r < W && c >= 0 && c < W) {
-                const C* src = onum + (size_t)k * P.onum_planes * WW + (size_t)r * W + c;
-                C v[kMaxBatchModes];                          // every plane's load in flight at once
+            for (int u = 0; u < U; ++u) {
+                const int t = t0 + u;
+                const int k = t < total ? list[t] : 0;
+                const int2 an = t < total ? lanc[t] : make_int2(0, 0);
 #pragma unroll
-                for (int m = 0; m < kMaxBatchModes; ++m)
-                    if (m < P.onum_planes) v[m] = src[(size_t)m * WW];
-                C s = v[0];
-#pragma unroll
-                for (int m = 1; m < kMaxBatchModes; ++m)
-                    if (m < P.onum_planes) s = s + v[m];     // mode order, as before
-                num[q] = num[q] + s;
-                den[q] += gamma * peak + (T(1) - gamma) * pp[(size_t)r * W + c];
+                for (int q = 0; q < PX; ++q) {
+                    const int p = threadIdx.x + q * 256, R = R0 + p / kObjTile, Cc = C0 + p % kObjTile;
+                    const int r = R - an.x, c = Cc - an.y;
+                    ok[u][q] = t < total && R < P.H && Cc < P.Wc && r >= 0 && r < W && c >= 0 && c < W;
+                    if (ok[u][q]) {
+                        const C* src = onum + (size_t)k * P.onum_planes * WW + (size_t)r * W + c;
+                        v[u][q] = src[0];
+                        pw[u][q] = pp[(size_t)r * W + c];
+                    }
+                }
             }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int q = 0; q < PX; ++q)
+                    if (ok[u][q]) {
+                        num[q] = num[q] + v[u][q];
+                        den[q] += gamma * peak + (T(1) - gamma) * pw[u][q];
+                    }
         }
-        k = kn;
-        ar = arn;
-        ac = acn;
+    };
+    if constexpr (ONE_PLANE) {
+        accumulate(std::integral_constant<int, 4>{});
+    } else {                                                  // per-mode planes (bk_rows_inv)
+        int k = list[0];
+        int2 an = lanc[0];
+        for (int t = 0; t < total; ++t) {
+            const int kn = t + 1 < total ? list[t + 1] : k;  // the next position's entry read ahead
+            const int2 ann = t + 1 < total ? lanc[t + 1] : an;
+#pragma unroll
+            for (int q = 0; q < PX; ++q) {
+                const int p = threadIdx.x + q * 256, R = R0 + p / kObjTile, Cc = C0 + p % kObjTile;
+                const int r = R - an.x, c = Cc - an.y;
+                if (R < P.H && Cc < P.Wc && r >= 0 && r < W && c >= 0 && c < W) {
+                    const C* src = onum + (size_t)k * P.onum_planes * WW + (size_t)r * W + c;
+                    C v[kMaxBatchModes];                      // every plane's load in flight at once
+#pragma unroll
+                    for (int m = 0; m < kMaxBatchModes; ++m)
+                        if (m < P.onum_planes) v[m] = src[(size_t)m * WW];
+                    C sm = v[0];
+#pragma unroll
+                    for (int m = 1; m < kMaxBatchModes; ++m)
+                        if (m < P.onum_planes) sm = sm + v[m];   // mode order
+                    num[q] = num[q] + sm;
+                    den[q] += gamma * peak + (T(1) - gamma) * pp[(size_t)r * W + c];
+                }
+            }
+            k = kn;
+            an = ann;
+        }
     }
 #pragma unroll
     for (int q = 0; q < PX; ++q) {

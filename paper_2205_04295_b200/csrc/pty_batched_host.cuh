@@ -38,7 +38,7 @@ struct BatchShape {
 // Positions per chunk (PTY_BATCH_CHUNK overrides).  Default: the whole batch,
 // capped by a device-memory budget for the per-position scratch and object
 // numerators (2 M W^2 complex each, PTY_BATCH_BUDGET_MB, default 8 GB) and by
-// the gather kernel's shared-memory position list (4 bytes per position), so
+// the gather kernel's shared-memory position list (12 bytes per position), so
 // a large batch_size runs in chunks instead of failing.
 inline int batch_chunk(int b, size_t per_pos_bytes = 0) {
     const int c = env_int("PTY_BATCH_CHUNK", 0);
@@ -49,9 +49,11 @@ inline int batch_chunk(int b, size_t per_pos_bytes = 0) {
         chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)chunk, budget / per_pos_bytes));
     }
     const size_t smem = max_dyn_smem();
-    if (smem > 1024) chunk = std::min(chunk, (int)((smem - 1024) / sizeof(int)));
+    if (smem > 1024) chunk = std::min(chunk, (int)((smem - 1024) / (3 * sizeof(int))));
     return std::max(1, chunk);
 }
+// bk_obj_gather's shared memory: position list + anchors (int + int2 each)
+inline size_t gather_smem(int chunk) { return (size_t)((chunk + 1) & ~1) * sizeof(int) + (size_t)chunk * sizeof(int2); }
 template <typename T> inline size_t batch_pos_bytes(int W, int M) { return (size_t)2 * M * W * W * sizeof(cplx<T>); }
 
 template <int W> inline int k4_groups(int chunk) {
@@ -152,9 +154,9 @@ template <typename T, int W>
 int run_batch_contrib_fused(const PtyBatchArgs* a, BatchDev& P, const BatchShape& sh, const BatchLayout& L, int S,
                             cudaStream_t st) {
     const int M = a->modes, b = a->n_batch;
-    const size_t s_gather = (size_t)sh.chunk * sizeof(int);
+    const size_t s_gather = gather_smem(sh.chunk);
     if (s_gather > max_dyn_smem()) return PTY_ERR_ARGUMENT;
-    int rc = set_smem(bk_obj_gather<T, W>, s_gather);
+    int rc = set_smem(bk_obj_gather<T, W, true>, s_gather);
     if (rc) return rc;
     const size_t HW = (size_t)a->H * a->Wc, WW = (size_t)W * W;
     cudaMemsetAsync(a->obj_acc, 0, 3 * HW * sizeof(T), st);
@@ -171,7 +173,7 @@ int run_batch_contrib_fused(const PtyBatchArgs* a, BatchDev& P, const BatchShape
         Q.batch = P.batch + off;
         Q.anchors = P.anchors + 2 * off;
         Q.visit0 = P.visit0 + off;
-        bk_obj_gather<T, W><<<sh.ntiles, 256, s_gather, st>>>(Q);
+        bk_obj_gather<T, W, true><<<sh.ntiles, 256, s_gather, st>>>(Q);
         launches += 1;
     }
     P.G = S;
@@ -197,7 +199,7 @@ int run_batch_contrib(const PtyBatchArgs* a, cudaStream_t st) {
     const size_t s_k1 = W * sizeof(C) + (kLineThreads / B) * XS * sizeof(C) + NTEAM * W * 5 * sizeof(C) + 64 * sizeof(T);
     const size_t s_k23 = W * sizeof(C) + (kLineThreads / B) * XS * sizeof(C);
     const size_t s_k4 = W * sizeof(C) + 4 * LS4 * sizeof(C) + 4 * W * sizeof(C) + 4 * W * sizeof(T);
-    const size_t s_gather = (size_t)sh.chunk * sizeof(int);
+    const size_t s_gather = gather_smem(sh.chunk);
     if (s_gather > max_dyn_smem() || s_k4 > max_dyn_smem()) return PTY_ERR_ARGUMENT;
     if ((rc = set_smem(bk_rows_fwd<T, W>, s_k1)) || (rc = set_smem(bk_cols_fwd<T, W>, s_k23)) ||
         (rc = set_smem(bk_cols_mod<T, W>, s_k23)) || (rc = set_smem(bk_rows_inv<T, W>, s_k4)) ||
