@@ -755,11 +755,88 @@ __device__ __forceinline__ T task_rows_inv_block(const cplx<T>* tw, cplx<T>* lin
             pk = fmax(pk, U.update_probe ? npp : ppk);
         }
     };
+#ifndef PTY_P4_NO_PAIRS
+    if constexpr (std::is_same<T, float>::value && W % 2 == 0) {
+        // fp32: a thread takes column pairs (c, c+1) of a row, so the probe
+        // (and staging) accesses are 16-byte loads / stores; the object patch
+        // sits at an arbitrary anchor, its accesses stay 8-byte
+        constexpr int HW2 = W / 2, NP = NE / 2, CP = CH / 2 > 0 ? CH / 2 : 1;
+#pragma unroll 1
+        for (int h = 0; h < NP; h += CP) {
+            C ov[2 * CP], pv[MODES][2 * CP];
+#pragma unroll
+            for (int k = 0; k < CP; ++k) {
+                const int q = tl + (h + k) * TEAM, rr = q / HW2, c = 2 * (q % HW2), r = RT * blk + rr;
+                const C* orow = obj + (size_t)(ar + r) * Wc + ac + c;
+                ov[2 * k] = orow[0];
+                ov[2 * k + 1] = orow[1];
+#pragma unroll
+                for (int m = 0; m < MODES; ++m) {
+                    const float4 v = *reinterpret_cast<const float4*>(probes + m * WW + (size_t)r * W + c);
+                    pv[m][2 * k] = C{v.x, v.y};
+                    pv[m][2 * k + 1] = C{v.z, v.w};
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < CP; ++k) {
+                const int q = tl + (h + k) * TEAM, rr = q / HW2, c0 = 2 * (q % HW2), r = RT * blk + rr;
+                C np2[MODES][2], no2[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int c = c0 + u;
+                    const C o = ov[2 * k + u];
+                    T dp = beta * omax + (T(1) - beta) * norm2(o);
+                    dp = dp + eps_rel * dmax_p;
+                    const T idp = rcp_fast(dp);
+                    const OMul<T> om(o);
+                    C numer{T(0), T(0)};
+                    T npp = T(0);
+#pragma unroll
+                    for (int m = 0; m < MODES; ++m) {
+                        const C pm = pv[m][2 * k + u];
+                        const C X = lines[(m * RT + rr) * LS + pad<W>(c)];
+                        const C d = scale(X, checker<T>(r, c) * invW2) - om.mul(pm);
+                        numer = numer + mulc(d, pm);
+                        np2[m][u] = pm;
+                        if (U.update_probe) {
+                            const C np_ = pm + scale(om.mulconj(scale(d, alpha_p)), idp);
+                            np2[m][u] = np_;
+                            npp += norm2(np_);
+                        }
+                    }
+                    T ppk = T(0);
+#pragma unroll
+                    for (int m = 0; m < MODES; ++m) ppk += norm2(pv[m][2 * k + u]);
+                    T den = gamma * peak + (T(1) - gamma) * ppk;
+                    den = den + eps_rel * dmax_o;
+                    const C no = o + scale(scale(numer, alpha_o), rcp_fast(den));
+                    obj[(size_t)(ar + r) * Wc + ac + c] = o + (no - o);      // paste_add_inplace
+                    no2[u] = no;
+                    pk = fmax(pk, U.update_probe ? npp : ppk);
+                }
+                if (U.update_probe) {
+#pragma unroll
+                    for (int m = 0; m < MODES; ++m)
+                        *reinterpret_cast<float4*>(probes + m * WW + (size_t)r * W + c0) =
+                            make_float4(np2[m][0].re, np2[m][0].im, np2[m][1].re, np2[m][1].im);
+                }
+                if (stg) {
+                    *reinterpret_cast<float4*>(stg + (size_t)r * W + c0) =
+                        make_float4(ov[2 * k].re, ov[2 * k].im, ov[2 * k + 1].re, ov[2 * k + 1].im);
+                    *reinterpret_cast<float4*>(stg + WW + (size_t)r * W + c0) =
+                        make_float4(no2[0].re, no2[0].im, no2[1].re, no2[1].im);
+                }
+            }
+        }
+    } else
+#endif
+    {
 #pragma unroll 1
     for (int h = 0; h < NE; h += CH) {
         C ov[CH], pv[MODES][CH];
         load_chunk(h, ov, pv);
         update_chunk(h, ov, pv);
+    }
     }
     PTY_PROBE_STAMP(14);
     pk = group_max<B>(pk);
