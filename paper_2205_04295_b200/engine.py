@@ -333,10 +333,23 @@ def update_probe(probe, o_j, psi_corrected, alpha_probe: float, beta: float,
     return out if _is_tensor(probe) else out.cpu().numpy()
 
 
+_ORDER_CACHE: dict = {}
+
+
 def visit_order(n: int, config: SolverConfig, iteration: int) -> np.ndarray:
-    """engine.py:177-181."""
+    """engine.py:177-181.  Shuffled orders are memoised (read-only arrays):
+    a replica sweep computes the next iteration's orders while its kernel
+    runs, so the host work between two sweeps does not include them."""
     if config.position_order == "shuffled":
-        return np.random.default_rng([config.shuffle_seed, iteration]).permutation(n)
+        key = (int(n), config.shuffle_seed, int(iteration))
+        perm = _ORDER_CACHE.get(key)
+        if perm is None:
+            perm = np.random.default_rng([config.shuffle_seed, iteration]).permutation(n)
+            perm.flags.writeable = False
+            if len(_ORDER_CACHE) >= 4096:
+                _ORDER_CACHE.clear()
+            _ORDER_CACHE[key] = perm
+        return perm
     return np.arange(n)
 
 
@@ -588,6 +601,7 @@ def sweep_replicas(states, datasets, config: SolverConfig, orders=None, kernel_e
     datasets = list(datasets)
     if len(states) != len(datasets) or not states:
         raise ParameterError("need one dataset per state")
+    configs = None
     if isinstance(config, (list, tuple)):
         configs = list(config)
         if len(configs) != len(states):
@@ -690,6 +704,9 @@ def sweep_replicas(states, datasets, config: SolverConfig, orders=None, kernel_e
         if (config.ortho_interval > 0 and st.probe_stack.shape[0] > 1
                 and (st.iteration + 1) % config.ortho_interval == 0):
             _native.orthogonalize(st.probe_stack)
+    # the next sweep's visit orders, computed while this one runs on the GPU
+    for st, c in zip(states, configs if configs is not None else [config] * len(states)):
+        visit_order(n, c, st.iteration + 1)
 
     rb["err_h"].copy_(rb["err_d"], non_blocking=True)
     rb["status_h"].copy_(rb["status_d"], non_blocking=True)
