@@ -393,7 +393,7 @@ CONFIGS = {
     "config3": dict(W=256, M=3, grid=(20, 20), step=32.0, radius=60.0, powers=(0.8, 0.1, 0.1), lam=8.3187e-10,
                     posref=True, propagator="farfield", replicas=18, distinct_data=True),
     "config4": dict(W=512, M=5, grid=(40, 40), step=64.0, radius=120.0, powers=(0.8, 0.05, 0.05, 0.05, 0.05),
-                    lam=8.29e-10, posref=True, propagator="fresnel", replicas=6, distinct_data=False),
+                    lam=8.29e-10, posref=True, propagator="fresnel", replicas=9, distinct_data=False),
 }
 
 
