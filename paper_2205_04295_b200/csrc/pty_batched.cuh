@@ -26,6 +26,9 @@
 namespace pty {
 
 constexpr int kBatThreads = 128;
+#ifndef PTY_GATHER_U
+#define PTY_GATHER_U 1          // covering positions per round in the one-plane gather (1 / 2 / 4 / 8: 18.86 / 18.92 / 19.37 / 21.13 ms per config-5 sweep)
+#endif
 constexpr int kObjTile = 32;           // owner tile edge (canvas pixels)
 constexpr int kMaxBatchModes = 8;
 
@@ -378,8 +381,8 @@ __global__ void __launch_bounds__(256) bk_obj_gather(const __grid_constant__ Bat
 #pragma unroll
     for (int q = 0; q < PX; ++q) { num[q] = C{T(0), T(0)}; den[q] = T(0); }
     // one numerator plane per position (the line-task pass): covering positions
-    // in batch order, U at a time -- their numerator and sum|P|^2 loads fly
-    // together, the sums are added in list order
+    // in batch order, U at a time (their numerator and sum|P|^2 loads fly
+    // together; more than one per round costs occupancy), added in list order
     auto accumulate = [&](auto u_const) {
         constexpr int U = decltype(u_const)::value;
         for (int t0 = 0; t0 < total; t0 += U) {
@@ -414,7 +417,7 @@ __global__ void __launch_bounds__(256) bk_obj_gather(const __grid_constant__ Bat
         }
     };
     if constexpr (ONE_PLANE) {
-        accumulate(std::integral_constant<int, 4>{});
+        accumulate(std::integral_constant<int, PTY_GATHER_U>{});
     } else {                                                  // per-mode planes (bk_rows_inv)
         int k = list[0];
         int2 an = lanc[0];
