@@ -182,3 +182,20 @@ def test_batched_line_task_flavour_vs_chain_and_oracle(gpu, monkeypatch):
             assert res["1"][1] < res["0"][1]
         else:                                     # complex128 row blocks exceed shared memory: the chain
             assert res["1"][1] == res["0"][1]
+
+
+def test_l2_persistence_window_is_bitwise_neutral(gpu, monkeypatch):
+    """PTY_L2_PERSIST_MB (an L2 access-policy window over the sweep scratch)
+    changes only cache residency: 6 replicas of the benchmarked shape give the
+    same bits with and without it."""
+    runs = []
+    for mb in ("0", "32"):
+        monkeypatch.setenv("PTY_L2_PERSIST_MB", mb)
+        dsets = [scene(256, 3, (3, 3), 32.0, 60.0, seed=11 + r) for r in range(6)]
+        cfgs = [pk.SolverConfig(alpha_obj=0.9, alpha_probe=0.9, beta=0.5, gamma=0.5, mode_count=3,
+                                precision="fp32", init_seed=r, shuffle_seed=100 + r) for r in range(6)]
+        states = [pk.initialize(d, c) for d, c in zip(dsets, cfgs)]
+        pk.sweep_replicas(states, dsets, cfgs)
+        runs.append([(s.obj.cpu().numpy(), s.probe_stack.cpu().numpy(), list(s.error_trace)) for s in states])
+    for a, b in zip(*runs):
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2]
