@@ -360,6 +360,13 @@ int run_sweep_batched(const BatchedSweepIO& io, cudaStream_t st) {
     int rc = plan_lines_grid<T, W, true>(M, S, P, L, grid, smem);
     if (rc) return rc;
     if (!P.slot_local || !P.p4_staged || !P.resident) return kBatchedNoFit;
+    // no SM pairing here: with three slot barriers per step the paired
+    // anti-phase start measured slower (config 5: 18.80-18.94 vs 18.42-18.45
+    // ms per sweep unpaired); PTY_BATCH_SLOT_PAIR=1 restores it
+    if (!env_int("PTY_BATCH_SLOT_PAIR", 0)) {
+        P.pair = 0;
+        P.pair_offset = 0;
+    }
     if (cudaMemsetAsync(L.barrier, 0, sizeof(unsigned int), st) != cudaSuccess) return PTY_ERR_CUDA;
     if (cudaMemsetAsync(L.slot_bar, 0, (size_t)S * 32 * sizeof(unsigned int), st) != cudaSuccess) return PTY_ERR_CUDA;
     if (cudaMemsetAsync(L.sm_pair, 0, (8 + 256) * sizeof(unsigned int), st) != cudaSuccess) return PTY_ERR_CUDA;
